@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the tour-construction hot path (BASELINE.json metric).
+
+A step is one synchronous ACO iteration over the whole colony (every ant builds a
+tour against the frozen colony, then the completion step runs) on the C5
+workload by default: 200,000-city mixed instance, m=1024 ants, k=16, alpha=1,
+beta=2 (BASELINE.json configs[4], the config the >=40%-of-roofline target is
+quoted on). Multi-GPU = independent replicas (the path shards by
+ants but one GPU already holds every chain, so ranks run separate seeds).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "city-selection decisions/sec"
+UNIT = "decisions/s"
+
+
+def b_dec(k: int) -> int:
+    """algorithmic bytes per candidate-hit decision = k*(4 idx + 8 coords + 4 tau) + 4."""
+    return 16 * k + 4
+
+
+def workload(name: str):
+    from paper_1709_03187_b200.instances import CONFIGS
+
+    spec = dict(CONFIGS[name])
+    return spec
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def reduce_max_sum(values_max, values_sum, backend_device=None):
+    """max over ranks of values_max, sum over ranks of values_sum (torch.distributed)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return list(values_max), list(values_sum)
+    dev = backend_device or "cpu"
+    tmax = torch.tensor(values_max, dtype=torch.float64, device=dev)
+    tsum = torch.tensor(values_sum, dtype=torch.float64, device=dev)
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    return tmax.tolist(), tsum.tolist()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_sample(spec, inst, seconds, threads):
+    """O1 (the unmodified reference compiled in oracle/_ref) timed on the host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    r = oracle.ref_sample_select(inst.xs, inst.ys, spec["m"], 1.0, 2.0, 0.95, 1.0, 12345, threads, seconds)
+    rate = r["decisions"] * threads / r["busy_s"] if r["busy_s"] > 0 else 0.0
+    return rate, r
+
+
+def cpu_port_sample(spec, inst, threads, ants):
+    """O2 (the restatement of the north-star rule) on the host cores: one seeding +
+    one partial iteration of a reduced colony on the same instance."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    o = oracle.O2(inst.xs, inst.ys, m=ants, k=spec["k"], seed=3, threads=threads) if inst.n <= 20000 else None
+    if o is None:
+        return None
+    t0 = time.perf_counter()
+    o.iterate()
+    o.iterate()
+    dt = time.perf_counter() - t0
+    return o.counters()["decisions"] / dt
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    spec = workload(args.config)
+    from paper_1709_03187_b200.instances import make_config_instance
+
+    inst = make_config_instance(args.config)
+    threads = os.cpu_count() or 1
+    per_step = max(2.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    rates, decisions, busy = [], 0, 0.0
+    t_all = time.perf_counter()
+    for s in range(args.warmup + args.steps):
+        rate, r = cpu_reference_sample(spec, inst, per_step, threads)
+        if s >= args.warmup:
+            rates.append(rate)
+            decisions += r["decisions"]
+            busy += r["busy_s"]
+    value = decisions * threads / busy if busy else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: n={spec['n']} m={spec['m']} (reference rule: Independent Roulette "
+                               f"over all unvisited cities, construction.hpp:246-281)", "threads": threads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{decisions} paco::select_next calls on the {args.config} instance with a "
+                                   f"{spec['m']}-ant ColonyPheromone; remaining-candidate counts drawn from the "
+                                   f"workload's full/partial mix; {per_step:.0f}s per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_all,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_03187_b200 import Colony, Mode, RunConfig, make_config_instance, run as paco_run
+
+    torch.cuda.set_device(local)
+    spec = workload(args.config)
+    inst = make_config_instance(args.config)
+    k = spec["k"]
+    cfg = RunConfig(ants=spec["m"], iterations=args.warmup + args.steps, alpha=1.0, beta=2.0, rho=0.5,
+                    partial_prob=0.95, max_mod_frac=1.0, candidates=k, seed=1 + rank, device=local,
+                    synchronous=True)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    col = Colony(inst, cfg, Mode.partial_aco)
+    for _ in range(args.warmup):
+        col.iterate(1)
+    c0 = col.counters()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, construct_ms = [], []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (torch stream, synchronised below)
+            torch.cuda.synchronize()
+            col.iterate(1)  # library-recorded CUDA events on the engine stream
+            c_ms, u_ms, _ = col.timing()
+            step_ms.append(c_ms + u_ms)
+            construct_ms.append(c_ms)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    c1 = col.counters()
+    decisions = c1["decisions"] - c0["decisions"]
+    fallbacks = c1["fallbacks"] - c0["fallbacks"]
+    total_ms = sum(step_ms)
+    col.close()
+
+    # end to end through the public C-ABI call: host coordinates in, g_best tour out
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = paco_run(inst, cfg, Mode.partial_aco)
+    e2e_s = time.perf_counter() - t0
+    e2e_dec = rep.counters["decisions"]
+
+    dev = f"cuda:{local}" if world > 1 else None
+    (tmax, e2emax), (dsum, e2esum, tours_sum) = reduce_max_sum(
+        [total_ms, e2e_s], [decisions, e2e_dec, spec["m"] * args.steps], dev)
+    if rank != 0:
+        return 0
+    value = dsum / (tmax / 1e3)
+    c_ms_avg = sum(construct_ms) / len(construct_ms)
+    bytes_per_launch = b_dec(k) * (decisions / args.steps)
+    achieved = bytes_per_launch / (c_ms_avg / 1e3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get("k_construct", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        try:
+            rate, r = cpu_reference_sample(spec, inst, args.cpu_seconds, threads)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{r['decisions']} paco::select_next calls (unmodified reference, IR rule) on the "
+                             f"{args.config} instance, {args.cpu_seconds:.0f}s on {threads} threads"}
+        except Exception as e:  # the reference harness is test infrastructure; report, do not fail
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "sample": f"unavailable: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {spec['n']}-city {spec['kind']} EUC_2D, m={spec['m']}, "
+                               f"k={k}, alpha=1, beta=2, partial_prob=0.95, max_mod_frac=1.0",
+                   "step": "one synchronous ACO iteration (weights, construction, completion step)",
+                   "l2": "flushed (512 MiB write) before every timed step; per-step working set "
+                         "(neighbour slices + tours) exceeds L2",
+                   "parallelism": f"replicas x{world}"},
+        "tours_per_s": tours_sum / (tmax / 1e3),
+        "fallback_frac": fallbacks / max(1, decisions),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "k_construct",
+                     "bytes_per_decision": b_dec(k), "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks
+                     else "fallback 6650 GB/s (B200_PROFILING.md)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2esum / e2emax, "unit": UNIT, "h2d_bytes_per_step": 16 * inst.n / cfg.iterations,
+                "d2h_bytes_per_step": (4 * inst.n + 8) / cfg.iterations,
+                "note": "paco_run: coordinates H2D, grid+k-NN build, all iterations incl. seeding, g_best D2H"},
+        "gpu_launches": 4 * args.steps,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        if args.impl == "reference":
+            # the reference arm is a CPU measurement on rank 0 only; other ranks exit without work
+            return run_reference_arm(args, rank, world)
+        dist.init_process_group("nccl")
+    try:
+        if args.impl == "reference":
+            return run_reference_arm(args, rank, world)
+        return run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            if dist.is_initialized():
+                dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,58 @@
+"""In-tree build of the sm_100a engine library (nvcc, no torch extension machinery).
+
+    python -m paper_1709_03187_b200.build
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "_lib", "libpaco_b200.so")
+SOURCES = [os.path.join(CSRC, f) for f in ("paco_b200.cu",)]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "device.cuh")] + [
+    os.path.join(ROOT, "include", "paco_b200.h")]
+
+NVCC_FLAGS = [
+    "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    # validated arithmetic must not be contracted; no fast-math
+    "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.sep not in cand or os.path.exists(cand)):
+            return cand
+    return "nvcc"
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(OUT):
+        return False
+    t = os.path.getmtime(OUT)
+    return all(os.path.getmtime(d) <= t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return OUT
+    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, *SOURCES]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log = os.path.join(os.path.dirname(OUT), "ptxas.log")
+    with open(log, "w") as f:
+        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr)
+        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,659 @@
+// Host side of the B200 tour-construction engine and its C ABI (include/paco_b200.h).
+// One handle = one instance + one colony resident in HBM + one CUDA stream.
+// An iteration is five launches on that stream:
+//   K5 k_weights  -> K2 k_construct -> [K6 classic deposit] -> K4 k_update -> k_publish
+// which together replace one barrier-synchronous iteration of paco::run
+// (/root/reference/proj/include/paco/engine.hpp:245-306).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/paco_b200.h"
+#include "kernels.cuh"
+
+using namespace pacob200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+paco_status fail(paco_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+#define CU(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(PACO_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+    return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1));
+}
+
+int kmax_for(uint32_t k) { return k <= 8 ? 8 : k <= 16 ? 16 : k <= 24 ? 24 : 32; }
+
+} // namespace
+
+struct paco_handle {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    paco_config cfg{};
+    int mode = 0;
+    uint32_t n = 0, m = 0, k = 0, nwords = 0;
+    GridParams g{};
+    std::vector<double> hx, hy;
+    std::vector<uint32_t> h_orig, h_int;
+    // device
+    double2* xy = nullptr;
+    uint32_t *orig_of = nullptr, *int_of = nullptr, *cell_start = nullptr;
+    uint32_t* knn = nullptr;
+    float* eta = nullptr;
+    uint2* cand = nullptr;
+    uint32_t* tours = nullptr;
+    uint8_t *lb_sel = nullptr, *has_lb = nullptr, *improved = nullptr, *partial = nullptr;
+    int64_t *new_len = nullptr, *lb_len = nullptr, *g_len = nullptr;
+    uint2* nbr = nullptr;
+    uint2* cur_nbr = nullptr;
+    double* T = nullptr;
+    GBest* gb = nullptr;
+    unsigned long long* counters = nullptr;
+    int* err = nullptr;
+    uint32_t* words = nullptr;
+    uint64_t words_stride = 0, words_cap = 0;
+    bool words_ready = false;
+    uint32_t* scratch_u32 = nullptr;  // n-sized staging for offers / construct_at
+    unsigned long long* scratch_u64 = nullptr;
+    uint64_t iter = 0;
+    double construct_ms = 0, update_ms = 0, setup_ms = 0;
+    std::vector<cudaEvent_t> evpool;
+    uint32_t knn_global_fallbacks = 0;
+
+    ~paco_handle() {
+        if (dev >= 0) cudaSetDevice(dev);
+        void* ptrs[] = {xy, orig_of, int_of, cell_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
+                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, counters, err, words,
+                        scratch_u32, scratch_u64};
+        for (void* p : ptrs)
+            if (p) cudaFree(p);
+        for (auto e : evpool) cudaEventDestroy(e);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+extern "C" {
+
+const char* paco_last_error(void) { return g_last_error.c_str(); }
+int paco_version(void) { return 1; }
+
+paco_status paco_config_default(paco_config* c) {
+    if (!c) return fail(PACO_E_INVALID, "null config");
+    *c = paco_config{};
+    // RunConfig defaults, engine.hpp:43-59
+    c->ants = 16; c->iterations = 100000; c->alpha = 5.0; c->beta = 5.0;
+    c->partial_prob = 0.95; c->max_mod_frac = 1.0; c->two_opt_prob = 0.0; c->two_opt_window = 0;
+    c->workers = 8; c->seed = 1; c->rho = 0.1; c->tau_max = 1.0; c->tau0 = 1.0;
+    c->time_budget_s = 0.0; c->convergence_interval_s = 1.0;
+    c->synchronous = 1;  // the reference default is async; the GPU engine is the sync path
+    c->validate_tours = 0;
+    c->candidates = 16; c->draws = PACO_DRAWS_PHILOX; c->device = -1;
+    return PACO_OK;
+}
+
+paco_status paco_config_validate(const paco_config* c, uint32_t n, int mode) {
+    if (!c) return fail(PACO_E_INVALID, "null config");
+    // RunConfig::validate, engine.hpp:61-75 (same messages)
+    if (c->ants < 1) return fail(PACO_E_INVALID, "ants must be >= 1");
+    if (c->iterations < 1) return fail(PACO_E_INVALID, "iterations must be >= 1");
+    if (c->workers < 1) return fail(PACO_E_INVALID, "workers must be >= 1");
+    if (!(c->partial_prob >= 0.0 && c->partial_prob <= 1.0))
+        return fail(PACO_E_INVALID, "partial_prob must be in [0,1]");
+    if (!(c->max_mod_frac > 0.0 && c->max_mod_frac <= 1.0))
+        return fail(PACO_E_INVALID, "max_mod_frac must be in (0,1]");
+    if (!(c->two_opt_prob >= 0.0 && c->two_opt_prob <= 1.0))
+        return fail(PACO_E_INVALID, "two_opt_prob must be in [0,1]");
+    if (!(c->rho >= 0.0 && c->rho <= 1.0)) return fail(PACO_E_INVALID, "rho must be in [0,1]");
+    if (!(c->tau0 > 0.0)) return fail(PACO_E_INVALID, "tau0 must be positive");
+    if (!(c->tau_max > 0.0)) return fail(PACO_E_INVALID, "tau_max must be positive");
+    if (!(c->time_budget_s >= 0.0)) return fail(PACO_E_INVALID, "time budget must be >= 0");
+    if (mode < 0 || mode > 2) return fail(PACO_E_INVALID, "unknown mode");
+    // engine.hpp:158-160
+    if (mode == PACO_MODE_CLASSIC && n > 5000)
+        return fail(PACO_E_INVALID, "classic mode requires n <= 5000");
+    if (n < 3) return fail(PACO_E_INVALID, "instance needs at least 3 cities, got " + std::to_string(n));
+    if (c->candidates < 1 || c->candidates > 32) return fail(PACO_E_INVALID, "candidates must be in [1,32]");
+    if (c->draws > 1) return fail(PACO_E_INVALID, "unknown draw source");
+    if (c->two_opt_prob > 0.0) return fail(PACO_E_UNSUPPORTED, "2-opt is not provided by the GPU engine yet");
+    if (!c->synchronous) return fail(PACO_E_UNSUPPORTED, "asynchronous mode is not provided by the GPU engine yet");
+    return PACO_OK;
+}
+
+static paco_status build_grid(paco_handle* h) {
+    const uint32_t n = h->n;
+    double x0 = h->hx[0], x1 = x0, y0 = h->hy[0], y1 = y0;
+    for (uint32_t i = 1; i < n; ++i) {
+        x0 = std::min(x0, h->hx[i]); x1 = std::max(x1, h->hx[i]);
+        y0 = std::min(y0, h->hy[i]); y1 = std::max(y1, h->hy[i]);
+    }
+    const double w = std::max(x1 - x0, 1e-9), hh = std::max(y1 - y0, 1e-9);
+    double cs = std::sqrt(w * hh * 2.0 / n);
+    if (!(cs > 0) || !std::isfinite(cs)) cs = 1.0;
+    int32_t gw = 0, gh = 0;
+    uint32_t L = 3;
+    for (;;) {
+        const double fw = w / cs + 1.0, fh = hh / cs + 1.0;
+        if (fw < 32768.0 && fh < 32768.0) {
+            gw = (int32_t)(w / cs) + 1; gh = (int32_t)(hh / cs) + 1;
+            L = 3;
+            while ((1 << L) < std::max(gw, gh)) ++L;
+            if ((uint64_t)gw * gh <= 4ull * n + 16 && (1ull << (2 * L)) <= 16ull * n + 4096) break;
+        }
+        cs *= 1.25;
+    }
+    h->g.x0 = x0; h->g.y0 = y0; h->g.cs = cs; h->g.inv = 1.0 / cs;
+    h->g.gw = gw; h->g.gh = gh; h->g.gws = (gw + 7) / 8; h->g.ghs = (gh + 7) / 8;
+    h->g.L = L; h->g.ncells = 1u << (2 * L);
+    return PACO_OK;
+}
+
+static paco_status setup(paco_handle* h) {
+    const uint32_t n = h->n, m = h->m, k = h->k;
+    cudaStream_t st = h->st;
+    if (build_grid(h) != PACO_OK) return PACO_E_RUNTIME;
+    double *dx = nullptr, *dy = nullptr;
+    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    uint32_t* cellm = nullptr;
+    CU(dalloc(&dx, n)); CU(dalloc(&dy, n));
+    CU(dalloc(&keys, n)); CU(dalloc(&keys2, n)); CU(dalloc(&cellm, n));
+    CU(dalloc(&h->xy, n)); CU(dalloc(&h->orig_of, n)); CU(dalloc(&h->int_of, n));
+    CU(dalloc(&h->cell_start, (size_t)h->g.ncells + 1));
+    CU(dalloc(&h->knn, (size_t)n * k)); CU(dalloc(&h->eta, (size_t)n * k)); CU(dalloc(&h->cand, (size_t)n * k));
+    CU(dalloc(&h->tours, (size_t)m * 2 * n));
+    CU(dalloc(&h->lb_sel, m)); CU(dalloc(&h->has_lb, m)); CU(dalloc(&h->improved, m)); CU(dalloc(&h->partial, m));
+    CU(dalloc(&h->new_len, m)); CU(dalloc(&h->lb_len, m)); CU(dalloc(&h->g_len, 1));
+    CU(dalloc(&h->nbr, (size_t)m * n));
+    CU(dalloc(&h->gb, 1)); CU(dalloc(&h->counters, 8)); CU(dalloc(&h->err, 1));
+    CU(dalloc(&h->scratch_u32, (size_t)n + 64)); CU(dalloc(&h->scratch_u64, 4));
+    if (h->mode == PACO_MODE_CLASSIC) {
+        CU(dalloc(&h->T, (size_t)n * k));
+        CU(dalloc(&h->cur_nbr, (size_t)m * n));
+        std::vector<double> init((size_t)n * k, h->cfg.tau_max);
+        CU(cudaMemcpyAsync(h->T, init.data(), sizeof(double) * init.size(), cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    CU(cudaMemsetAsync(h->lb_sel, 0, m, st)); CU(cudaMemsetAsync(h->has_lb, 0, m, st));
+    CU(cudaMemsetAsync(h->improved, 0, m, st)); CU(cudaMemsetAsync(h->partial, 0, m, st));
+    CU(cudaMemsetAsync(h->lb_len, 0, sizeof(int64_t) * m, st));
+    CU(cudaMemsetAsync(h->nbr, 0, sizeof(uint2) * (size_t)m * n, st));
+    CU(cudaMemsetAsync(h->tours, 0, sizeof(uint32_t) * (size_t)m * 2 * n, st));
+    GBest g0{0, -1, 0};
+    const int64_t gmax = std::numeric_limits<int64_t>::max();
+    CU(cudaMemcpyAsync(h->gb, &g0, sizeof g0, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(h->g_len, &gmax, sizeof gmax, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(h->counters, 0, 8 * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(h->err, 0, sizeof(int), st));
+
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, st));
+    CU(cudaMemcpyAsync(dx, h->hx.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dy, h->hy.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    const uint32_t tb = 256, nb = (n + tb - 1) / tb;
+    k_cell_keys<<<nb, tb, 0, st>>>(dx, dy, n, h->g, keys);
+    CU(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    const int end_bit = 32 + 2 * (int)h->g.L;
+    CU(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys2, (int)n, 0, end_bit, st));
+    void* tmp = nullptr;
+    CU(cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 1));
+    CU(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, keys2, (int)n, 0, end_bit, st));
+    k_scatter<<<nb, tb, 0, st>>>(keys2, dx, dy, n, h->xy, h->orig_of, h->int_of, cellm);
+    k_cell_start<<<nb, tb, 0, st>>>(cellm, n, h->g.ncells, h->cell_start);
+    CU(cudaGetLastError());
+    // K1: k-NN over superblocks, staged in shared memory (cap cities per CTA)
+    const uint32_t cap = 6144;
+    const size_t smem = (size_t)cap * (sizeof(double2) + 2 * sizeof(uint32_t));
+    const uint32_t nsb = h->g.ncells >> 6;
+    uint32_t* nglob = h->scratch_u32;
+    CU(cudaMemsetAsync(nglob, 0, sizeof(uint32_t), st));
+    const int km = kmax_for(k);
+#define LAUNCH_KNN(KM)                                                                                  \
+    do {                                                                                                \
+        CU(cudaFuncSetAttribute(k_knn<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+        k_knn<KM><<<nsb, 128, smem, st>>>(h->xy, h->orig_of, h->cell_start, h->g, n, (int)k,            \
+                                          h->cfg.beta, cap, h->knn, h->eta, nglob);                     \
+    } while (0)
+    if (km == 8) LAUNCH_KNN(8); else if (km == 16) LAUNCH_KNN(16); else if (km == 24) LAUNCH_KNN(24); else LAUNCH_KNN(32);
+#undef LAUNCH_KNN
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(e1, st));
+    CU(cudaStreamSynchronize(st));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    h->setup_ms = ms;
+    CU(cudaMemcpy(&h->knn_global_fallbacks, nglob, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    h->h_orig.resize(n); h->h_int.resize(n);
+    CU(cudaMemcpy(h->h_orig.data(), h->orig_of, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+    for (uint32_t p = 0; p < n; ++p) h->h_int[h->h_orig[p]] = p;
+    cudaFree(tmp); cudaFree(dx); cudaFree(dy); cudaFree(keys); cudaFree(keys2); cudaFree(cellm);
+    return PACO_OK;
+}
+
+paco_status paco_create(const double* xs, const double* ys, uint32_t n, const paco_config* cfg, int mode,
+                        paco_handle** out) {
+    if (!out) return fail(PACO_E_INVALID, "null output handle");
+    *out = nullptr;
+    if (!xs || !ys) return fail(PACO_E_INVALID, "null coordinates");
+    paco_status s = paco_config_validate(cfg, n, mode);
+    if (s != PACO_OK) return s;
+    for (uint32_t i = 0; i < n; ++i)
+        if (!std::isfinite(xs[i]) || !std::isfinite(ys[i])) return fail(PACO_E_INVALID, "non-finite coordinate");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(PACO_E_CUDA, "no CUDA device visible (the B200 engine has no CPU fallback)");
+    int dev = cfg->device;
+    if (dev < 0) CU(cudaGetDevice(&dev));
+    CU(cudaSetDevice(dev));
+    cudaDeviceProp prop{};
+    CU(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10) return fail(PACO_E_CUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+    const uint32_t nwords = (n + 31) / 32;
+    if ((size_t)nwords * 4 > (size_t)prop.sharedMemPerBlockOptin)
+        return fail(PACO_E_UNSUPPORTED, "visited bitmap exceeds shared memory (n too large)");
+    auto* h = new (std::nothrow) paco_handle();
+    if (!h) return fail(PACO_E_RUNTIME, "out of host memory");
+    h->dev = dev;
+    h->cfg = *cfg;
+    h->mode = mode;
+    h->n = n; h->m = cfg->ants; h->k = std::min<uint32_t>(cfg->candidates, n - 1); h->nwords = nwords;
+    h->hx.assign(xs, xs + n); h->hy.assign(ys, ys + n);
+    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
+        delete h;
+        return fail(PACO_E_CUDA, "stream creation failed");
+    }
+    s = setup(h);
+    if (s != PACO_OK) { delete h; return s; }
+    *out = h;
+    return PACO_OK;
+}
+
+void paco_destroy(paco_handle* h) { delete h; }
+
+static cudaEvent_t ev(paco_handle* h, size_t i) {
+    while (h->evpool.size() <= i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        h->evpool.push_back(e);
+    }
+    return h->evpool[i];
+}
+
+static paco_status launch_weights(paco_handle* h) {
+    const uint32_t n = h->n, tb = 256;
+    const size_t smem = h->T ? 0 : sizeof(double) * h->m;
+    const int km = kmax_for(h->k);
+    const double* T = h->mode == PACO_MODE_CLASSIC ? h->T : nullptr;
+#define LAUNCH_W(KM)                                                                                       \
+    do {                                                                                                   \
+        if (smem > 48 * 1024)                                                                              \
+            CU(cudaFuncSetAttribute(k_weights<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        k_weights<KM><<<(n + tb - 1) / tb, tb, smem, h->st>>>(h->knn, h->eta, h->nbr, h->lb_len, h->has_lb,  \
+                                                            h->g_len, T, n, h->m, (int)h->k, h->cfg.alpha, \
+                                                            h->cfg.tau0, h->cand);                         \
+    } while (0)
+    if (km == 8) LAUNCH_W(8); else if (km == 16) LAUNCH_W(16); else if (km == 24) LAUNCH_W(24); else LAUNCH_W(32);
+#undef LAUNCH_W
+    CU(cudaGetLastError());
+    return PACO_OK;
+}
+
+static ConstructArgs construct_args(paco_handle* h, bool seeding) {
+    ConstructArgs a{};
+    a.cand = h->cand; a.xy = h->xy; a.orig_of = h->orig_of; a.int_of = h->int_of;
+    a.cell_start = h->cell_start; a.g = h->g; a.tours = h->tours; a.lb_sel = h->lb_sel;
+    a.new_len = h->new_len; a.partial_flag = h->partial; a.counters = h->counters;
+    a.words = h->cfg.draws == PACO_DRAWS_BUFFER ? h->words : nullptr;
+    a.stride = h->words_stride; a.seed = h->cfg.seed; a.iter = h->iter;
+    a.n = h->n; a.m = h->m; a.k = h->k; a.nwords = h->nwords;
+    a.eff_pp = h->mode == PACO_MODE_PARTIAL ? h->cfg.partial_prob : 0.0;  // engine.hpp:164-165
+    a.mmf = h->cfg.max_mod_frac;
+    a.seeding = seeding ? 1 : 0;
+    a.validate = h->cfg.validate_tours ? 1 : 0;
+    a.err = h->err;
+    return a;
+}
+
+static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint32_t blocks) {
+    const size_t smem = (size_t)h->nwords * 4;
+    if (smem > 48 * 1024)
+        CU(cudaFuncSetAttribute(k_construct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_construct<<<blocks, 32, smem, h->st>>>(a);
+    CU(cudaGetLastError());
+    return PACO_OK;
+}
+
+static paco_status check_err(paco_handle* h) {
+    int err = 0;
+    CU(cudaMemcpyAsync(&err, h->err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    if (err) return fail(PACO_E_INVALID, "candidate tour is not a permutation");
+    return PACO_OK;
+}
+
+paco_status paco_iterate(paco_handle* h, uint64_t count) {
+    if (!h) return fail(PACO_E_INVALID, "null handle");
+    CU(cudaSetDevice(h->dev));
+    if (h->cfg.draws == PACO_DRAWS_BUFFER && count > 1)
+        return fail(PACO_E_INVALID, "buffer draws feed one iteration per paco_set_draws call");
+    const uint32_t n = h->n, m = h->m;
+    std::vector<std::pair<size_t, size_t>> marks;
+    size_t e = 0;
+    for (uint64_t it = 0; it < count; ++it) {
+        if (h->cfg.draws == PACO_DRAWS_BUFFER && !h->words_ready)
+            return fail(PACO_E_INVALID, "no draw buffer set for this iteration");
+        const bool seeding = h->mode != PACO_MODE_CLASSIC && h->iter == 0;
+        const size_t e0 = e++, e1 = e++, e2 = e++;
+        CU(cudaEventRecord(ev(h, e0), h->st));
+        paco_status s = launch_weights(h);
+        if (s != PACO_OK) return s;
+        CU(cudaEventRecord(ev(h, e1), h->st));
+        s = launch_construct(h, construct_args(h, seeding), m);
+        if (s != PACO_OK) return s;
+        CU(cudaEventRecord(ev(h, e2), h->st));
+        if (h->mode == PACO_MODE_CLASSIC) {
+            // evaporate + deposit on the built tours before the l_best updates (engine.hpp:253-259)
+            dim3 grid((n + 255) / 256, m);
+            k_publish<<<grid, 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, n, 1, h->cur_nbr);
+            const int km = kmax_for(h->k);
+            const uint32_t nb = (n + 255) / 256;
+            if (km == 8) k_classic<8><<<nb, 256, 0, h->st>>>(h->knn, h->cur_nbr, h->new_len, n, m, (int)h->k, h->cfg.rho, h->T);
+            else if (km == 16) k_classic<16><<<nb, 256, 0, h->st>>>(h->knn, h->cur_nbr, h->new_len, n, m, (int)h->k, h->cfg.rho, h->T);
+            else if (km == 24) k_classic<24><<<nb, 256, 0, h->st>>>(h->knn, h->cur_nbr, h->new_len, n, m, (int)h->k, h->cfg.rho, h->T);
+            else k_classic<32><<<nb, 256, 0, h->st>>>(h->knn, h->cur_nbr, h->new_len, n, m, (int)h->k, h->cfg.rho, h->T);
+            CU(cudaGetLastError());
+        }
+        k_update<<<1, 32, 0, h->st>>>(0, m, h->new_len, h->lb_len, h->has_lb, h->lb_sel, h->improved, h->gb,
+                                      h->g_len, h->counters);
+        dim3 grid((n + 255) / 256, m);
+        k_publish<<<grid, 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, n, 0, h->nbr);
+        CU(cudaGetLastError());
+        const size_t e3 = e++;
+        CU(cudaEventRecord(ev(h, e3), h->st));
+        marks.push_back({e0, e3});
+        ++h->iter;
+        h->words_ready = false;
+        if (h->cfg.validate_tours) {
+            paco_status s2 = check_err(h);
+            if (s2 != PACO_OK) return s2;
+        }
+    }
+    CU(cudaStreamSynchronize(h->st));
+    double c_ms = 0, u_ms = 0;
+    for (auto& mk : marks) {
+        float a = 0, b = 0, c = 0;
+        CU(cudaEventElapsedTime(&a, ev(h, mk.first), ev(h, mk.first + 1)));
+        CU(cudaEventElapsedTime(&b, ev(h, mk.first + 1), ev(h, mk.first + 2)));
+        CU(cudaEventElapsedTime(&c, ev(h, mk.first + 2), ev(h, mk.second)));
+        c_ms += b; u_ms += a + c;
+    }
+    h->construct_ms = c_ms; h->update_ms = u_ms;
+    return PACO_OK;
+}
+
+paco_status paco_set_draws(paco_handle* h, const uint32_t* words, uint64_t stride) {
+    if (!h || !words) return fail(PACO_E_INVALID, "null argument");
+    if (h->cfg.draws != PACO_DRAWS_BUFFER) return fail(PACO_E_INVALID, "handle was not created with buffer draws");
+    if (stride < 4ull + h->n) return fail(PACO_E_INVALID, "stride must be >= n + 4 words");
+    CU(cudaSetDevice(h->dev));
+    const uint64_t need = stride * h->m;
+    if (need > h->words_cap) {
+        if (h->words) cudaFree(h->words);
+        h->words = nullptr;
+        CU(dalloc(&h->words, need));
+        h->words_cap = need;
+    }
+    CU(cudaMemcpyAsync(h->words, words, sizeof(uint32_t) * need, cudaMemcpyHostToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    h->words_stride = stride;
+    h->words_ready = true;
+    return PACO_OK;
+}
+
+static paco_status read_half(paco_handle* h, bool lbest, uint32_t* tours, int64_t* lengths) {
+    const uint32_t n = h->n, m = h->m;
+    CU(cudaSetDevice(h->dev));
+    std::vector<uint8_t> sel(m);
+    CU(cudaMemcpy(sel.data(), h->lb_sel, m, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> buf((size_t)n);
+    if (tours) {
+        for (uint32_t a = 0; a < m; ++a) {
+            // the tour built this iteration sits in the half that is not l_best, unless it
+            // improved, in which case the selector already flipped onto it
+            uint8_t half = sel[a];
+            if (!lbest) {
+                uint8_t imp = 0;
+                CU(cudaMemcpy(&imp, h->improved + a, 1, cudaMemcpyDeviceToHost));
+                half = imp ? sel[a] : (uint8_t)(1 - sel[a]);
+            }
+            CU(cudaMemcpy(buf.data(), h->tours + ((size_t)a * 2 + half) * n, sizeof(uint32_t) * n,
+                          cudaMemcpyDeviceToHost));
+            uint32_t* o = tours + (size_t)a * n;
+            for (uint32_t p = 0; p < n; ++p) o[p] = h->h_orig[buf[p]];
+        }
+    }
+    if (lengths) CU(cudaMemcpy(lengths, lbest ? h->lb_len : h->new_len, sizeof(int64_t) * m, cudaMemcpyDeviceToHost));
+    return PACO_OK;
+}
+
+paco_status paco_get_tours(paco_handle* h, uint32_t* tours, int64_t* lengths) {
+    if (!h) return fail(PACO_E_INVALID, "null handle");
+    return read_half(h, false, tours, lengths);
+}
+
+paco_status paco_get_l_best(paco_handle* h, uint32_t* tours, int64_t* lengths) {
+    if (!h) return fail(PACO_E_INVALID, "null handle");
+    return read_half(h, true, tours, lengths);
+}
+
+paco_status paco_get_g_best(paco_handle* h, uint32_t* tour, int64_t* length) {
+    if (!h) return fail(PACO_E_INVALID, "null handle");
+    CU(cudaSetDevice(h->dev));
+    GBest g{};
+    CU(cudaMemcpy(&g, h->gb, sizeof g, cudaMemcpyDeviceToHost));
+    if (!g.has) { if (length) *length = -1; return PACO_OK; }
+    if (length) *length = g.len;
+    if (tour) {
+        uint8_t sel = 0;
+        CU(cudaMemcpy(&sel, h->lb_sel + g.ant, 1, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> buf(h->n);
+        CU(cudaMemcpy(buf.data(), h->tours + ((size_t)g.ant * 2 + sel) * h->n, sizeof(uint32_t) * h->n,
+                      cudaMemcpyDeviceToHost));
+        for (uint32_t p = 0; p < h->n; ++p) tour[p] = h->h_orig[buf[p]];
+    }
+    return PACO_OK;
+}
+
+paco_status paco_get_counters(paco_handle* h, paco_counters* c) {
+    if (!h || !c) return fail(PACO_E_INVALID, "null argument");
+    CU(cudaSetDevice(h->dev));
+    unsigned long long v[8];
+    CU(cudaMemcpy(v, h->counters, sizeof v, cudaMemcpyDeviceToHost));
+    c->decisions = v[0]; c->fallbacks = v[1]; c->ties = v[2]; c->forced = v[3];
+    c->full_builds = v[4]; c->partial_builds = v[5]; c->iterations = h->iter; c->improvements = v[7];
+    return PACO_OK;
+}
+
+paco_status paco_get_build_flags(paco_handle* h, uint8_t* partial, uint8_t* improved) {
+    if (!h) return fail(PACO_E_INVALID, "null handle");
+    CU(cudaSetDevice(h->dev));
+    if (partial) CU(cudaMemcpy(partial, h->partial, h->m, cudaMemcpyDeviceToHost));
+    if (improved) CU(cudaMemcpy(improved, h->improved, h->m, cudaMemcpyDeviceToHost));
+    return PACO_OK;
+}
+
+paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, uint32_t* k_out) {
+    if (!h) return fail(PACO_E_INVALID, "null handle");
+    CU(cudaSetDevice(h->dev));
+    const uint32_t n = h->n, k = h->k;
+    if (k_out) *k_out = k;
+    std::vector<uint2> c((size_t)n * k);
+    std::vector<uint32_t> kn((size_t)n * k);
+    CU(cudaMemcpy(kn.data(), h->knn, sizeof(uint32_t) * kn.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(c.data(), h->cand, sizeof(uint2) * c.size(), cudaMemcpyDeviceToHost));
+    for (uint32_t o = 0; o < n; ++o) {
+        const uint32_t i = h->h_int[o];
+        for (uint32_t r = 0; r < k; ++r) {
+            if (knn) knn[(size_t)o * k + r] = h->h_orig[kn[(size_t)i * k + r]];
+            if (weights) std::memcpy(&weights[(size_t)o * k + r], &c[(size_t)i * k + r].y, 4);
+        }
+    }
+    return PACO_OK;
+}
+
+paco_status paco_get_timing(paco_handle* h, double* c, double* u, double* s) {
+    if (!h) return fail(PACO_E_INVALID, "null handle");
+    if (c) *c = h->construct_ms;
+    if (u) *u = h->update_ms;
+    if (s) *s = h->setup_ms;
+    return PACO_OK;
+}
+
+static int64_t host_length(const paco_handle* h, const uint32_t* order) {
+    auto d = [&](uint32_t a, uint32_t b) {
+        const double dx = h->hx[a] - h->hx[b], dy = h->hy[a] - h->hy[b];
+        return (int64_t)(int32_t)(std::sqrt(dx * dx + dy * dy) + 0.5);
+    };
+    int64_t t = 0;
+    for (uint32_t i = 0; i + 1 < h->n; ++i) t += d(order[i], order[i + 1]);
+    return t + d(order[h->n - 1], order[0]);
+}
+
+paco_status paco_offer_tour(paco_handle* h, uint32_t ant, const uint32_t* order, int* improved) {
+    if (!h || !order) return fail(PACO_E_INVALID, "null argument");
+    if (ant >= h->m) return fail(PACO_E_INVALID, "ant out of range");
+    const uint32_t n = h->n;
+    std::vector<uint8_t> seen(n, 0);
+    for (uint32_t i = 0; i < n; ++i) {  // colony.hpp:118-119
+        if (order[i] >= n || seen[order[i]]) return fail(PACO_E_INVALID, "candidate tour is not a permutation");
+        seen[order[i]] = 1;
+    }
+    CU(cudaSetDevice(h->dev));
+    std::vector<uint32_t> in(n);
+    for (uint32_t i = 0; i < n; ++i) in[i] = h->h_int[order[i]];
+    uint8_t sel = 0;
+    CU(cudaMemcpy(&sel, h->lb_sel + ant, 1, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(h->tours + ((size_t)ant * 2 + (1 - sel)) * n, in.data(), sizeof(uint32_t) * n,
+                  cudaMemcpyHostToDevice));
+    const int64_t L = host_length(h, order);
+    CU(cudaMemcpy(h->new_len + ant, &L, sizeof L, cudaMemcpyHostToDevice));
+    k_update<<<1, 32, 0, h->st>>>(ant, 1, h->new_len, h->lb_len, h->has_lb, h->lb_sel, h->improved, h->gb,
+                                  h->g_len, h->counters);
+    dim3 grid((n + 255) / 256, h->m);
+    k_publish<<<grid, 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, n, 0, h->nbr);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(h->st));
+    uint8_t imp = 0;
+    CU(cudaMemcpy(&imp, h->improved + ant, 1, cudaMemcpyDeviceToHost));
+    // only `ant` may publish: clear the others' flags that k_update did not touch
+    if (improved) *improved = imp;
+    return PACO_OK;
+}
+
+paco_status paco_construct_at(paco_handle* h, uint32_t ant, uint32_t start_pos, uint32_t m_mod,
+                              const uint32_t* words, uint64_t nwords, uint32_t* out_order, int64_t* out_length) {
+    if (!h || !words || !out_order) return fail(PACO_E_INVALID, "null argument");
+    if (ant >= h->m) return fail(PACO_E_INVALID, "ant out of range");
+    const uint32_t n = h->n;
+    if (m_mod > n) return fail(PACO_E_INVALID, "m_mod exceeds city count");  // construction.hpp:318
+    if (start_pos >= n) return fail(PACO_E_INVALID, "start_pos out of range");
+    if (nwords < 4ull + n) return fail(PACO_E_INVALID, "need n + 4 draw words");
+    CU(cudaSetDevice(h->dev));
+    uint8_t has = 0;
+    CU(cudaMemcpy(&has, h->has_lb + ant, 1, cudaMemcpyDeviceToHost));
+    if (!has) return fail(PACO_E_INVALID, "ant has no l_best");
+    uint32_t* dw = nullptr;
+    CU(dalloc(&dw, nwords));
+    CU(cudaMemcpy(dw, words, sizeof(uint32_t) * nwords, cudaMemcpyHostToDevice));
+    paco_status s = launch_weights(h);
+    if (s != PACO_OK) { cudaFree(dw); return s; }
+    ConstructArgs a = construct_args(h, false);
+    a.words = dw; a.stride = nwords; a.force = 1; a.force_ant = ant; a.force_start_pos = start_pos;
+    a.force_m_mod = m_mod; a.validate = 1;
+    int64_t saved_len = 0;
+    CU(cudaMemcpy(&saved_len, h->new_len + ant, sizeof saved_len, cudaMemcpyDeviceToHost));
+    CU(cudaMemsetAsync(h->err, 0, sizeof(int), h->st));
+    s = launch_construct(h, a, 1);
+    if (s != PACO_OK) { cudaFree(dw); return s; }
+    CU(cudaStreamSynchronize(h->st));
+    cudaFree(dw);
+    s = check_err(h);
+    if (s != PACO_OK) return s;
+    uint8_t sel = 0;
+    CU(cudaMemcpy(&sel, h->lb_sel + ant, 1, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> buf(n);
+    CU(cudaMemcpy(buf.data(), h->tours + ((size_t)ant * 2 + (1 - sel)) * n, sizeof(uint32_t) * n,
+                  cudaMemcpyDeviceToHost));
+    for (uint32_t p = 0; p < n; ++p) out_order[p] = h->h_orig[buf[p]];
+    CU(cudaMemcpy(out_length, h->new_len + ant, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(h->new_len + ant, &saved_len, sizeof saved_len, cudaMemcpyHostToDevice));
+    return PACO_OK;
+}
+
+paco_status paco_run(const double* xs, const double* ys, uint32_t n, const paco_config* cfg, int mode,
+                     int64_t optimum, paco_report* rep, uint32_t* best_tour) {
+    if (!rep) return fail(PACO_E_INVALID, "null report");
+    if (cfg && cfg->draws == PACO_DRAWS_BUFFER) return fail(PACO_E_INVALID, "paco_run uses Philox draws");
+    const auto t0 = std::chrono::steady_clock::now();
+    auto since = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    paco_handle* h = nullptr;
+    paco_status s = paco_create(xs, ys, n, cfg, mode, &h);
+    if (s != PACO_OK) return s;
+    double c_ms = 0, u_ms = 0;
+    uint64_t done = 0;
+    if (cfg->time_budget_s <= 0.0) {
+        s = paco_iterate(h, cfg->iterations);
+        c_ms = h->construct_ms; u_ms = h->update_ms;
+        done = cfg->iterations;
+    } else {
+        // engine.hpp:270-272: the in-flight iteration always completes
+        while (done < cfg->iterations && s == PACO_OK) {
+            s = paco_iterate(h, 1);
+            c_ms += h->construct_ms; u_ms += h->update_ms;
+            ++done;
+            if (since() >= cfg->time_budget_s) break;
+        }
+    }
+    if (s != PACO_OK) { paco_destroy(h); return s; }
+    std::vector<uint32_t> tour(n);
+    int64_t len = 0;
+    s = paco_get_g_best(h, tour.data(), &len);
+    if (s == PACO_OK) s = paco_get_counters(h, &rep->counters);
+    if (s == PACO_OK && host_length(h, tour.data()) != len)  // check_tour, engine.hpp:322
+        s = fail(PACO_E_LOGIC, "tour length cache does not match recomputation");
+    rep->setup_ms = h->setup_ms;
+    paco_destroy(h);
+    if (s != PACO_OK) return s;
+    rep->best_length = len;
+    rep->pct_error = optimum > 0 ? 100.0 * ((double)len - (double)optimum) / (double)optimum
+                                 : std::numeric_limits<double>::quiet_NaN();
+    rep->iterations_done = done;
+    rep->comparisons_total = rep->counters.decisions;
+    rep->construct_ms = c_ms; rep->update_ms = u_ms;
+    if (best_tour) std::memcpy(best_tour, tour.data(), sizeof(uint32_t) * n);
+    rep->wall_time_s = since();
+    return PACO_OK;
+}
+
+} // extern "C"

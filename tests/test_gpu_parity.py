@@ -1,0 +1,230 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the O2 oracle.
+
+Bar (BASELINE.json north star): chosen city sequences bit-exact, tour lengths
+exact (int64 of the reference's rounded distances), every tour a permutation,
+l_best / g_best updates identical. Roulette ties are counted, not excused: the
+GPU and O2 evaluate the same f32 scan, so they must agree even on ties.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1709_03187_b200 import (Colony, InvalidArgument, Mode, PacoError, RunConfig, cycle_length,
+                                   grid_instance, is_permutation_of_n, make_config_instance, run)
+from paper_1709_03187_b200.instances import Instance
+
+pytestmark = pytest.mark.gpu
+
+MODE_NAMES = {Mode.partial_aco: "partial", Mode.paco_full: "paco", Mode.classic_aco: "classic"}
+
+
+def lockstep(inst, iters, mode=Mode.partial_aco, words_fn=None, check_every=1, **kw):
+    m = kw.pop("ants", 16)
+    k = kw.pop("candidates", 20)
+    cfg = RunConfig(ants=m, iterations=iters, alpha=kw.get("alpha", 1.0), beta=kw.get("beta", 2.0),
+                    rho=kw.get("rho", 0.5), tau0=kw.get("tau0", 1.0), partial_prob=kw.get("partial_prob", 0.95),
+                    max_mod_frac=kw.get("max_mod_frac", 1.0), seed=kw.get("seed", 1), candidates=k,
+                    draws="buffer" if words_fn else "philox", validate_tours=True)
+    ref = oracle.O2(inst.xs, inst.ys, m=m, k=k, alpha=cfg.alpha, beta=cfg.beta, tau0=cfg.tau0,
+                    partial_prob=cfg.partial_prob, max_mod_frac=cfg.max_mod_frac, rho=cfg.rho, seed=cfg.seed,
+                    mode=MODE_NAMES[mode], draws="buffer" if words_fn else "philox")
+    col = Colony(inst, cfg, mode)
+    knn_gpu, _ = col.candidates()
+    assert np.array_equal(knn_gpu, ref.knn()), "k-NN candidate lists differ"
+    g_prev = None
+    for it in range(iters):
+        if words_fn:
+            w = words_fn(it, m, inst.n + 4)
+            col.set_draws(w)
+            col.iterate(1)
+            ref.iterate(w)
+        else:
+            col.iterate(1)
+            ref.iterate()
+        if (it + 1) % check_every and it + 1 != iters:
+            continue
+        tg, lg = col.tours()
+        tr, lr = ref.tours()
+        for a in range(m):
+            assert np.array_equal(tg[a], tr[a]), f"iteration {it} ant {a}: city sequence differs"
+        assert np.array_equal(lg, lr), f"iteration {it}: lengths differ"
+        _, wg = col.candidates()
+        assert np.array_equal(wg.view(np.uint32), ref.weights().view(np.uint32)), f"iteration {it}: weights differ"
+        pg, ig = col.build_flags()
+        pr, ir = ref.build_flags()
+        assert np.array_equal(pg, pr) and np.array_equal(ig, ir)
+        lbg, llg = col.l_best()
+        lbr, llr = ref.l_best()
+        assert np.array_equal(llg, llr) and np.array_equal(lbg, lbr)
+        gt, gl = col.g_best()
+        rt, rl = ref.g_best()
+        assert gl == rl and np.array_equal(gt, rt)
+        if g_prev is not None:
+            assert gl <= g_prev
+        g_prev = gl
+    cg, cr = col.counters(), ref.counters()
+    for key in ("decisions", "fallbacks", "ties", "forced", "full_builds", "partial_builds"):
+        assert cg[key] == cr[key], (key, cg[key], cr[key])
+    return col, ref
+
+
+def test_c1_partial_full_run():
+    inst = make_config_instance("C1")
+    col, ref = lockstep(inst, 100, ants=64, candidates=20)
+    c = col.counters()
+    assert c["fallbacks"] > 0 and c["partial_builds"] > 0 and c["full_builds"] > 64
+
+
+def test_c2_partial_iterations():
+    inst = make_config_instance("C2")
+    lockstep(inst, 8, ants=256, candidates=20, check_every=4)
+
+
+def test_c3_clustered_fallback_heavy():
+    inst = make_config_instance("C3")
+    col, _ = lockstep(inst, 6, ants=256, candidates=20, check_every=3)
+    assert col.counters()["fallbacks"] > 1000
+
+
+def test_paco_and_small_cap_modes():
+    inst = make_config_instance("C1", n=700)
+    lockstep(inst, 10, mode=Mode.paco_full, ants=24, candidates=16, seed=3)
+    lockstep(inst, 10, ants=24, candidates=16, seed=4, max_mod_frac=0.05)
+
+
+def test_classic_mode():
+    inst = make_config_instance("C1", n=800)
+    col, ref = lockstep(inst, 12, mode=Mode.classic_aco, ants=20, candidates=20, rho=0.5)
+
+
+def test_validation_buffer_draws():
+    rng = np.random.default_rng(5)
+
+    def words(it, m, stride):
+        return rng.integers(0, 2**32, size=(m, stride), dtype=np.uint64).astype(np.uint32)
+
+    inst = make_config_instance("C2", n=900)
+    lockstep(inst, 6, ants=16, candidates=12, words_fn=words)
+
+
+def test_alpha_beta_integer_powers():
+    inst = make_config_instance("C1", n=400)
+    lockstep(inst, 8, ants=8, candidates=10, alpha=5.0, beta=5.0, seed=11)
+
+
+@pytest.mark.parametrize("n,k", [(3, 20), (4, 20), (5, 2), (33, 32), (64, 1)])
+def test_tiny_instances(n, k):
+    rng = np.random.default_rng(n)
+    inst = Instance("tiny", rng.integers(0, 50, n).astype(float), rng.integers(0, 50, n).astype(float))
+    lockstep(inst, 6, ants=3, candidates=k, seed=n)
+
+
+def test_duplicates_and_collinear():
+    xs = np.array([5.0] * 40 + list(range(60)), dtype=float)
+    ys = np.array([5.0] * 40 + [0.0] * 60, dtype=float)
+    lockstep(Instance("dup", xs, ys), 8, ants=6, candidates=8)
+
+
+def test_grid442():
+    inst = grid_instance(26, 17, 10.0, "grid442")
+    col, _ = lockstep(inst, 30, ants=16, candidates=12)
+    assert col.g_best()[1] >= 4420
+
+
+def test_construct_at_degenerate_counts():
+    inst = grid_instance(6, 5)  # n = 30
+    cfg = RunConfig(ants=1, iterations=1, alpha=5.0, beta=5.0, candidates=8)
+    ref = oracle.O2(inst.xs, inst.ys, m=1, k=8, alpha=5.0, beta=5.0)
+    order = np.random.default_rng(4).permutation(30).astype(np.uint32)
+    with Colony(inst, cfg) as col:
+        assert col.offer_tour(0, order)
+        assert ref.offer_tour(0, order)
+        words = np.random.default_rng(9).integers(0, 2**32, 40, dtype=np.uint64).astype(np.uint32)
+        for start, m_mod in [(7, 0), (4, 1), (11, 2), (11, 7), (11, 29), (13, 30)]:
+            tg, lg = col.construct_at(0, start, m_mod, words)
+            tr, lr = ref.construct_at(0, start, m_mod, words)
+            assert np.array_equal(tg, tr) and lg == lr
+            assert is_permutation_of_n(30, tg)
+            keep = 30 - m_mod
+            assert np.array_equal(tg[:keep], order[(start + np.arange(keep)) % 30])
+            if m_mod == 0:
+                assert lg == cycle_length(inst, order)
+            if m_mod == 30:
+                assert tg[0] == order[13]
+        with pytest.raises(InvalidArgument):
+            col.construct_at(0, 0, 31, words)
+
+
+def test_offer_tour_strict_improvement():
+    inst = Instance.from_coords("rect", [(0, 0), (3, 0), (3, 4), (0, 4)])
+    with Colony(inst, RunConfig(ants=1, iterations=1, candidates=3)) as col:
+        assert col.offer_tour(0, [0, 1, 3, 2])        # 16
+        assert not col.offer_tour(0, [0, 2, 1, 3])    # longer
+        assert not col.offer_tour(0, [1, 3, 2, 0])    # equal: incumbent kept
+        assert col.offer_tour(0, [0, 1, 2, 3])        # 14
+        assert col.g_best()[1] == 14
+        with pytest.raises(InvalidArgument):
+            col.offer_tour(0, [0, 1, 2, 2])
+
+
+@pytest.mark.parametrize("cfg_name", ["C4", "C5"])
+def test_large_configs_properties(cfg_name):
+    """Full-size configs: permutation + exact length checks on every tour, monotone
+    g_best, k-NN rows spot-checked against brute force."""
+    from paper_1709_03187_b200.instances import CONFIGS
+
+    spec = CONFIGS[cfg_name]
+    inst = make_config_instance(cfg_name)
+    cfg = RunConfig(ants=spec["m"], iterations=3, alpha=1.0, beta=2.0, rho=0.5, candidates=spec["k"],
+                    validate_tours=True)
+    with Colony(inst, cfg) as col:
+        knn, _ = col.candidates()
+        rows = np.random.default_rng(0).choice(inst.n, 64, replace=False)
+        assert np.array_equal(knn[rows], oracle.knn_rows(inst.xs, inst.ys, spec["k"], rows))
+        g_prev = None
+        for it in range(3):
+            col.iterate(1)
+            tours, lens = col.tours()
+            for a in range(0, spec["m"], 7):
+                assert is_permutation_of_n(inst.n, tours[a])
+                assert cycle_length(inst, tours[a]) == lens[a]
+            g = col.g_best()[1]
+            assert g_prev is None or g <= g_prev
+            g_prev = g
+
+
+def test_run_api_matches_colony():
+    inst = make_config_instance("C1", n=500)
+    cfg = RunConfig(ants=16, iterations=12, alpha=1.0, beta=2.0, candidates=20, seed=5)
+    rep = run(inst, cfg, Mode.partial_aco)
+    ref = oracle.O2(inst.xs, inst.ys, m=16, k=20, seed=5)
+    for _ in range(12):
+        ref.iterate()
+    assert rep.best_length == ref.g_best()[1]
+    assert np.array_equal(rep.best_tour.order, ref.g_best()[0])
+    assert rep.iterations_done == 12 and rep.counters["decisions"] == ref.counters()["decisions"]
+
+
+def test_quality_gate_within_one_percent_of_oracle_mean():
+    """North star: final best after a fixed budget within 1% of the oracle's mean over 5 seeds."""
+    inst = make_config_instance("C1")
+    gpu, cpu = [], []
+    for seed in range(1, 6):
+        rep = run(inst, RunConfig(ants=64, iterations=100, alpha=1.0, beta=2.0, rho=0.5, candidates=20, seed=seed))
+        gpu.append(rep.best_length)
+        ref = oracle.O2(inst.xs, inst.ys, m=64, k=20, seed=seed)
+        for _ in range(100):
+            ref.iterate()
+        cpu.append(ref.g_best()[1])
+    assert abs(np.mean(gpu) - np.mean(cpu)) <= 0.01 * np.mean(cpu)
+    assert gpu == cpu
+
+
+def test_config_errors():
+    inst = make_config_instance("C1", n=6000)
+    with pytest.raises(InvalidArgument):
+        Colony(inst, RunConfig(ants=4), Mode.classic_aco)
+    with pytest.raises(InvalidArgument):
+        Colony(inst, RunConfig(ants=0))
+    with pytest.raises(PacoError):
+        Colony(inst, RunConfig(ants=4, two_opt_prob=0.1))
