@@ -108,7 +108,7 @@ void o2_knn_rows(const double* xs, const double* ys, uint32_t n, uint32_t k,
 
 /* Roulette over one candidate list, as one warp computes it: lane l holds w[l]
  * (0 for lanes >= k), five Hillis-Steele steps v[l] += v[l-off] in f32, total
- * S = v[k-1], target = u*S, pick = lowest lane with v > target, else the last
+ * S = v[k-1], target = u*S, pick = lowest feasible lane with v > target, else the last
  * lane with w > 0. Returns -1 when S == 0 (every candidate visited). */
 int32_t o2_roulette(const float* w, uint32_t k, uint32_t word, int32_t* tie) {
     float v[32], nv[32];
@@ -124,8 +124,10 @@ int32_t o2_roulette(const float* w, uint32_t k, uint32_t word, int32_t* tie) {
     const float tol = 1e-6f * S;
     for (uint32_t l = 0; l < k; ++l)
         if (fabsf(v[l] - target) <= tol) { *tie = 1; break; }
+    /* feasible lanes only: the tree-shaped f32 scan is not monotone, so an
+       infeasible lane (w = 0) can carry S_r one ulp above S_{r-1} */
     for (uint32_t l = 0; l < k; ++l)
-        if (v[l] > target) return (int32_t)l;
+        if (w[l] > 0.0f && v[l] > target) return (int32_t)l;
     for (int32_t l = (int32_t)k - 1; l >= 0; --l)
         if (w[l] > 0.0f) return l;
     return -1;

@@ -19,7 +19,7 @@
  * North-star additions (no reference code; defined in DESIGN.md §3):
  *   - k-NN candidate lists ordered by (d^2, original index)
  *   - roulette over the list: f32 weights, 32-lane Hillis-Steele inclusive scan
- *     simulated lane by lane, pick = lowest lane with S_r > u*S (ballot), clamp
+ *     simulated lane by lane, pick = lowest feasible lane with S_r > u*S (ballot), clamp
  *     to last feasible lane
  *   - exact nearest-unvisited fallback, key (d^2, original index)
  *   - counter-based Philox4x32-10 draw schedule (slot layout in DESIGN.md)

@@ -11,7 +11,7 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8, c_uint32, c_uint64
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libpaco_b200.so")
+LIB_PATH = os.environ.get("PACO_B200_LIB") or os.path.join(LIB_DIR, "libpaco_b200.so")
 
 PACO_OK = 0
 PACO_E_RUNTIME = -1

@@ -449,6 +449,14 @@ __global__ void __launch_bounds__(32) k_construct(ConstructArgs a) {
         if (remaining == 1) {
             next = last_unvisited(vis, nw, lane);
             ++n_forced;
+#ifdef PACO_DEBUG
+            {
+                uint32_t zeros = 0;
+                for (uint32_t w = lane; w < nw; w += 32) zeros += __popc(~vis[w]);
+                for (int off = 16; off; off >>= 1) zeros += __shfl_xor_sync(kFull, zeros, off);
+                if (lane == 0 && zeros != 1) printf("DBG ant %u pos %u forced: zeros=%u next=%u\n", ant, pos, zeros, next);
+            }
+#endif
         } else {
             uint32_t uw;
             if (a.words) uw = a.words[(a.force ? 0 : (uint64_t)ant * a.stride) + 4 + t];
@@ -473,7 +481,9 @@ __global__ void __launch_bounds__(32) k_construct(ConstructArgs a) {
                 const float tol = __fmul_rn(1e-6f, S);
                 const bool in = lane < k;
                 if (__any_sync(kFull, in && fabsf(__fsub_rn(v, target)) <= tol)) ++n_tie;
-                unsigned ball = __ballot_sync(kFull, in && v > target);
+                // only feasible lanes may win: the tree-shaped scan is not monotone in f32,
+                // so an infeasible lane's S_r can exceed its left neighbour's by an ulp
+                unsigned ball = __ballot_sync(kFull, in && w > 0.0f && v > target);
                 int r;
                 if (ball) r = __ffs(ball) - 1;
                 else r = 31 - __clz(__ballot_sync(kFull, in && w > 0.0f));
@@ -483,6 +493,17 @@ __global__ void __launch_bounds__(32) k_construct(ConstructArgs a) {
                 ++n_fb;
             }
         }
+#ifdef PACO_DEBUG
+        {
+            const uint32_t nx0 = __shfl_sync(kFull, next, 0);
+            if (!__all_sync(kFull, nx0 == next) && lane == 0) printf("DBG ant %u pos %u non-uniform next\n", ant, pos);
+            if (is_visited(vis, next)) {
+                for (uint32_t q = lane; q < pos; q += 32)
+                    if (out[q] == next) printf("DBG ant %u pos %u dup next=%u rem=%u earlier at %u (partial=%d start_pos=%u m_mod=%u)\n", ant, pos, next, remaining, q, (int)partial, start_pos, m_mod);
+                if (lane == 0) printf("DBG ant %u pos %u dup next=%u word=%08x\n", ant, pos, next, vis[next >> 5]);
+            }
+        }
+#endif
         if (lane == 0) { out[pos] = next; vis[next >> 5] |= 1u << (next & 31); }
         __syncwarp();
         ++pos;
