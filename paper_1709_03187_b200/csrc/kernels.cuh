@@ -4,6 +4,9 @@
 #include "device.cuh"
 
 namespace pacob200 {
+#ifdef PACO_TIMING
+__device__ unsigned long long g_timing[16];
+#endif
 
 // ============================================================ K0: spatial sort
 // key = morton(cell) << 32 | original index; sorted by cub (one-time setup).
@@ -101,13 +104,13 @@ __device__ void knn_ring_search(uint32_t i, double2 q, const double2* __restrict
 }
 
 template <int KMAX>
-__device__ void knn_emit(uint32_t i, double2 q, const TopK<KMAX>& t, int k, const double2* __restrict__ xy,
-                         double beta, uint32_t* __restrict__ knn, float* __restrict__ eta) {
+__device__ void knn_emit(uint32_t i, double2 q, const TopK<KMAX>& t, int kk, int k, const double2* __restrict__ xy,
+                         double beta, uint32_t* __restrict__ knn32, float* __restrict__ eta) {
 #pragma unroll
     for (int r = 0; r < KMAX; ++r) {
+        const uint32_t jj = r < kk ? t.j[r] : kNone;
+        knn32[(size_t)i * KMAX + r] = jj;
         if (r < k) {
-            const uint32_t jj = t.j[r];
-            knn[(size_t)i * k + r] = jj;
             int32_t d = euc2d(q, xy[jj]);
             if (d < 1) d = 1;
             eta[(size_t)i * k + r] = (float)power(beta, 1.0 / (double)d);
@@ -118,7 +121,7 @@ __device__ void knn_emit(uint32_t i, double2 q, const TopK<KMAX>& t, int k, cons
 template <int KMAX>
 __global__ void __launch_bounds__(128) k_knn(const double2* __restrict__ xy, const uint32_t* __restrict__ orig_of,
                                              const uint32_t* __restrict__ cell_start, GridParams g, uint32_t n,
-                                             int k, double beta, uint32_t cap, uint32_t* __restrict__ knn,
+                                             int kk, int k, double beta, uint32_t cap, uint32_t* __restrict__ knn32,
                                              float* __restrict__ eta, uint32_t* __restrict__ n_global) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t sb = blockIdx.x;
@@ -169,22 +172,22 @@ __global__ void __launch_bounds__(128) k_knn(const double2* __restrict__ xy, con
             t.init();
             for (uint32_t p = 0; p < C; ++p) {
                 if (sj[p] == i) continue;
-                t.offer(dist2(q, sxy[p]), so[p], sj[p], k);
+                t.offer(dist2(q, sxy[p]), so[p], sj[p], kk);
             }
             double lb = fmin(fmin(q.x - xlo, xhi - q.x), fmin(q.y - ylo, yhi - q.y));
-            if (C >= (uint32_t)k + 1) {
+            if (C >= (uint32_t)kk + 1) {
                 if (lb == inf) ok = true;  // the staged region is the whole instance
                 else {
                     lb -= 1e-6 * g.cs;
-                    ok = lb > 0 && lb * lb > t.d[k - 1];
+                    ok = lb > 0 && lb * lb > t.d[kk - 1];
                 }
             }
         }
         if (!ok) {
             atomicAdd(n_global, 1u);
-            knn_ring_search<KMAX>(i, q, xy, orig_of, cell_start, g, k, t);
+            knn_ring_search<KMAX>(i, q, xy, orig_of, cell_start, g, kk, t);
         }
-        knn_emit<KMAX>(i, q, t, k, xy, beta, knn, eta);
+        knn_emit<KMAX>(i, q, t, kk, k, xy, beta, knn32, eta);
     }
 }
 
@@ -196,11 +199,11 @@ __global__ void __launch_bounds__(128) k_knn(const double2* __restrict__ xy, con
 // Classic mode reads tau from the candidate-edge pheromone table T instead.
 // Output: packed {c_r, w} rows, the only table the construction kernel reads.
 template <int KMAX>
-__global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ knn, const float* __restrict__ eta,
+__global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ knn32, const float* __restrict__ eta,
                                                  const uint2* __restrict__ nbr, const int64_t* __restrict__ lb_len,
                                                  const uint8_t* __restrict__ has_lb, const int64_t* __restrict__ g_len,
                                                  const double* __restrict__ T, uint32_t n, uint32_t m, int k,
-                                                 double alpha, double tau0, uint2* __restrict__ cand) {
+                                                 int kp, double alpha, double tau0, uint2* __restrict__ cand) {
     extern __shared__ double ratio[];
     if (!T) {
         const double g = (double)*g_len;
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ kn
     uint32_t c[KMAX];
     double acc[KMAX];
 #pragma unroll
-    for (int r = 0; r < KMAX; ++r) { c[r] = r < k ? knn[(size_t)i * k + r] : kNone; acc[r] = 0.0; }
+    for (int r = 0; r < KMAX; ++r) { c[r] = r < k ? knn32[(size_t)i * 32 + r] : kNone; acc[r] = 0.0; }
     if (!T) {
         for (uint32_t a = 0; a < m; ++a) {
             const double ra = ratio[a];
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ kn
         if (r < k) {
             const double tau = T ? T[(size_t)i * k + r] : __dadd_rn(tau0, acc[r]);
             const float w = __fmul_rn((float)power(alpha, tau), eta[(size_t)i * k + r]);
-            cand[(size_t)i * k + r] = make_uint2(c[r], __float_as_uint(w));
+            cand[(size_t)i * kp + r] = make_uint2(c[r], __float_as_uint(w));
         }
     }
 }
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ kn
 // ============================================================ K2: construction
 struct ConstructArgs {
     const uint2* cand;        // n*k {city, f32 weight}
+    const uint32_t* knn32;    // n*32 nearest cities by (d^2, orig), kNone padded
     const double2* xy;        // internal coordinates
     const uint32_t* orig_of;  // internal -> original (fallback tie-break)
     const uint32_t* int_of;   // original -> internal (start city draw)
@@ -255,7 +259,7 @@ struct ConstructArgs {
     const uint32_t* words;    // validation draws: m rows of `stride` words (nullptr = Philox)
     uint64_t stride;
     uint64_t seed, iter;
-    uint32_t n, m, k, nwords;
+    uint32_t n, m, k, kp, nwords;  // kp = row stride of cand (k rounded up to even)
     double eff_pp, mmf;
     int seeding;
     int validate;
@@ -265,43 +269,44 @@ struct ConstructArgs {
     uint32_t force_ant, force_start_pos, force_m_mod;
 };
 
+__device__ __forceinline__ double rect_lb2(double2 q, double rx0, double ry0, double side, double slack) {
+    const double dx = fmax(0.0, fmax(rx0 - q.x, q.x - (rx0 + side)));
+    const double dy = fmax(0.0, fmax(ry0 - q.y, q.y - (ry0 + side)));
+    const double lb = sqrt(dx * dx + dy * dy) - slack;
+    return lb > 0 ? lb * lb : 0.0;
+}
+
+struct FbStats {
+#ifdef PACO_TIMING
+    long long searches = 0, rings = 0, sbs = 0, cities = 0;
+#endif
+};
+
 // Exact nearest unvisited city by (d^2, original index), warp-cooperative.
-// Phase 1: Chebyshev rings of fine cells around cur (radius <= 2). Phase 2: rings
-// of 8x8-cell superblocks with rectangle lower bounds, pruning fully visited
-// superblocks with the shared-memory bitmap and far cells with the running bound.
-__device__ __noinline__ uint32_t nearest_unvisited(const ConstructArgs& a, const uint32_t* vis, uint32_t cur,
-                                                   uint32_t lane) {
+// F0: the 32-nearest list is sorted by the same key, so its first unvisited entry
+//     is the answer whenever one exists (one 128-byte row, one ballot).
+// F1: rings of 8x8-cell superblocks (each a contiguous id range) around cur with
+//     rectangle lower bounds. A superblock with no unvisited city is skipped with
+//     the shared-memory bitmap; the others are scanned flat, 128 ids per pass
+//     (four bitmap words broadcast to the warp, one predicated coordinate load per
+//     unvisited lane), so one pass costs a single L2 round trip. One warp argmin
+//     per ring; the ring loop stops when the next ring's bound exceeds the best.
+__device__ __forceinline__ uint32_t nearest_unvisited(const ConstructArgs& a, const uint32_t* vis, uint32_t cur,
+                                                   uint32_t lane, FbStats& fs) {
+    {
+        const uint32_t c = ldg_u32(&a.knn32[(size_t)cur * 32 + lane]);
+        const unsigned b = __ballot_sync(kFull, c != kNone && !is_visited(vis, c));
+        if (b) return __shfl_sync(kFull, c, __ffs(b) - 1);
+    }
+#ifdef PACO_TIMING
+    ++fs.searches;
+#endif
     const GridParams& g = a.g;
     const double2 q = a.xy[cur];
     const int32_t cx = cell_coord(q.x, g.x0, g.inv, g.gw), cy = cell_coord(q.y, g.y0, g.inv, g.gh);
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
-    double bd = inf;
+    double bd = __longlong_as_double(0x7ff0000000000000LL);
     uint32_t bo = kNone, bj = kNone;
     const double slack = 1e-6 * g.cs;
-    constexpr int32_t R1 = 2;
-    for (int32_t rho = 0; rho <= R1 + 1; ++rho) {
-        if (rho >= 1) {
-            const double lb = (rho - 1) * g.cs - slack;
-            if (lb > 0 && lb * lb > bd) return bj;
-        }
-        if (rho > R1) break;
-        const int32_t cnt = rho == 0 ? 1 : 8 * rho;
-        for (int32_t c = lane; c < cnt; c += 32) {
-            int32_t x = cx, y = cy;
-            if (rho) ring_cell(rho, c, cx, cy, x, y);
-            if (x < 0 || y < 0 || x >= g.gw || y >= g.gh) continue;
-            const uint32_t m = morton((uint32_t)x, (uint32_t)y);
-            const uint32_t s = a.cell_start[m], e = a.cell_start[m + 1];
-            for (uint32_t j = s; j < e; ++j) {
-                if (is_visited(vis, j)) continue;
-                const double d = dist2(q, a.xy[j]);
-                const uint32_t o = a.orig_of[j];
-                if (key_less(d, o, bd, bo)) { bd = d; bo = o; bj = j; }
-            }
-        }
-        warp_argmin(bd, bo, bj);
-    }
-    // phase 2: superblock rings
     const int32_t sx = cx >> 3, sy = cy >> 3;
     const int32_t rmax = g.gws > g.ghs ? g.gws : g.ghs;
     const double span = 8.0 * g.cs;
@@ -310,60 +315,64 @@ __device__ __noinline__ uint32_t nearest_unvisited(const ConstructArgs& a, const
             const double lb = (rho - 1) * span - slack;
             if (lb > 0 && lb * lb > bd) break;
         }
+#ifdef PACO_TIMING
+        ++fs.rings;
+#endif
+        const double bound = bd;  // warp-uniform (argmin at the end of every ring)
         const int32_t cnt = rho == 0 ? 1 : 8 * rho;
         for (int32_t base = 0; base < cnt; base += 32) {
             const int32_t c = base + (int32_t)lane;
             bool cand = false;
-            uint32_t sbm = 0;
+            uint32_t rs = 0, re = 0;
             if (c < cnt) {
                 int32_t x = sx, y = sy;
                 if (rho) ring_cell(rho, c, sx, sy, x, y);
-                if (x >= 0 && y >= 0 && x < g.gws && y < g.ghs) {
-                    const double rx0 = g.x0 + x * span, rx1 = rx0 + span;
-                    const double ry0 = g.y0 + y * span, ry1 = ry0 + span;
-                    const double dx = fmax(0.0, fmax(rx0 - q.x, q.x - rx1));
-                    const double dy = fmax(0.0, fmax(ry0 - q.y, q.y - ry1));
-                    const double lb = sqrt(dx * dx + dy * dy) - slack;
-                    if (!(lb > 0 && lb * lb > bd)) {
-                        sbm = morton((uint32_t)x, (uint32_t)y);
-                        cand = range_has_unvisited(vis, a.cell_start[sbm << 6], a.cell_start[(sbm + 1) << 6]);
-                    }
+                if (x >= 0 && y >= 0 && x < g.gws && y < g.ghs &&
+                    !(rect_lb2(q, g.x0 + x * span, g.y0 + y * span, span, slack) > bound)) {
+                    const uint32_t sbm = morton((uint32_t)x, (uint32_t)y);
+                    rs = a.cell_start[sbm << 6];
+                    re = a.cell_start[(sbm + 1) << 6];
+                    cand = range_has_unvisited(vis, rs, re);
                 }
             }
             unsigned ball = __ballot_sync(kFull, cand);
             while (ball) {
                 const int src = __ffs(ball) - 1;
                 ball &= ball - 1;
-                const uint32_t sb = __shfl_sync(kFull, sbm, src);
-                const double bound = bd;  // warp-uniform at this point
-                // 64 cells of the superblock, two per lane, pruned by the running bound
-                for (uint32_t cc = lane; cc < 64; cc += 32) {
-                    const uint32_t cm = (sb << 6) | cc;
-                    const uint32_t s = a.cell_start[cm], e = a.cell_start[cm + 1];
-                    if (s >= e) continue;
-                    const int32_t x = (int32_t)compact16(cm), y = (int32_t)compact16(cm >> 1);
-                    const double rx0 = g.x0 + x * g.cs, rx1 = rx0 + g.cs;
-                    const double ry0 = g.y0 + y * g.cs, ry1 = ry0 + g.cs;
-                    const double dx = fmax(0.0, fmax(rx0 - q.x, q.x - rx1));
-                    const double dy = fmax(0.0, fmax(ry0 - q.y, q.y - ry1));
-                    const double lb = sqrt(dx * dx + dy * dy) - slack;
-                    if (lb > 0 && lb * lb > bound) continue;
-                    for (uint32_t j = s; j < e; ++j) {
-                        if (is_visited(vis, j)) continue;
-                        const double d = dist2(q, a.xy[j]);
-                        const uint32_t o = a.orig_of[j];
-                        if (key_less(d, o, bd, bo)) { bd = d; bo = o; bj = j; }
+                const uint32_t s = __shfl_sync(kFull, rs, src), e = __shfl_sync(kFull, re, src);
+#ifdef PACO_TIMING
+                ++fs.sbs;
+#endif
+                for (uint32_t j0 = s & ~31u; j0 < e; j0 += 128) {
+                    uint32_t jj[4];
+                    bool un[4];
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        jj[q4] = j0 + 32 * q4 + lane;
+                        const uint32_t wd = (j0 + 32 * q4 < e) ? vis[(j0 >> 5) + q4] : 0xffffffffu;
+                        un[q4] = jj[q4] >= s && jj[q4] < e && !((wd >> lane) & 1u);
                     }
+                    double d[4];
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        if (un[q4]) { d[q4] = dist2(q, a.xy[jj[q4]]); o[q4] = a.orig_of[jj[q4]]; }
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        if (un[q4] && key_less(d[q4], o[q4], bd, bo)) { bd = d[q4]; bo = o[q4]; bj = jj[q4]; }
+#ifdef PACO_TIMING
+                    fs.cities += un[0] + un[1] + un[2] + un[3];
+#endif
                 }
-                warp_argmin(bd, bo, bj);
             }
         }
+        warp_argmin(bd, bo, bj);
     }
     return bj;
 }
 
 // the single remaining unvisited city (forced final step)
-__device__ __noinline__ uint32_t last_unvisited(const uint32_t* vis, uint32_t nwords, uint32_t lane) {
+__device__ __forceinline__ uint32_t last_unvisited(const uint32_t* vis, uint32_t nwords, uint32_t lane) {
     for (uint32_t base = 0; base < nwords; base += 32) {
         const uint32_t w = base + lane;
         const uint32_t free_bits = w < nwords ? ~vis[w] : 0u;
@@ -377,21 +386,71 @@ __device__ __noinline__ uint32_t last_unvisited(const uint32_t* vis, uint32_t nw
     return kNone;
 }
 
+__device__ __forceinline__ uint2 lds_u64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void red_or_shared(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+// predicated 16-byte global->shared async copy (LDGSTS), L1-allocating
+__device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, bool cond) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 16;\n\t}" ::"r"(dst),
+                 "l"(src), "r"((uint32_t)cond));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+#ifdef PACO_TIMING
+#define PACO_CLOCK(var, dep) long long var; asm volatile("mov.u64 %0, %%clock64;" : "=l"(var) : "r"(dep))
+#else
+#define PACO_CLOCK(var, dep)
+#endif
+
 // One warp per ant (construction.hpp:283-365 with the north-star selection rule,
 // engine.hpp:129-148 draw order). The visited bitmap (n bits) lives in shared
-// memory; each decision is one coalesced 8-byte-per-lane load of the current
-// city's candidate row, a bitmap probe, a warp inclusive scan, a ballot and a
-// shuffle. Preserved-segment copy, tour length and the optional permutation
-// check are warp-parallel passes fused before/after the dependent chain.
-__global__ void __launch_bounds__(32) k_construct(ConstructArgs a) {
-    extern __shared__ uint32_t vis[];
+// memory. The dependent chain of one decision is:
+//   candidate row of the current city (8 B per lane, coalesced) -> bitmap probe
+//   -> warp inclusive scan -> ballot -> shuffle of the winner.
+// The row does not come from L2 on that chain: while a decision is being made,
+// every lane with a feasible candidate copies that candidate's row into a
+// per-warp shared-memory stage with LDGSTS (cp.async), so the next decision finds
+// its row on chip whichever candidate wins. Off-chain work (visited bit of the
+// city just entered, draw word, tour store, tie log) is scheduled around the
+// chain; Philox draws come 128 at a time, one 4-word block per lane, handed out
+// by shuffle. Preserved-segment copy, tour length and the optional permutation
+// check are warp-parallel passes fused before/after the chain.
+//
+// KP = row stride (k rounded up to even; 0 = generic runtime value), STEPS = scan
+// steps, BUF = draws from the validation buffer instead of Philox.
+template <int KP, int STEPS, bool BUF>
+__global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];  // [2][k][kp] row stage | bitmap
     const uint32_t lane = threadIdx.x;
     const uint32_t ant = a.force ? a.force_ant : blockIdx.x;
     const uint32_t n = a.n, k = a.k, nw = a.nwords;
+    const uint32_t kp = KP ? (uint32_t)KP : a.kp;
+    const uint32_t slot_bytes = kp * 8, buf_bytes = k * slot_bytes;
+#ifdef PACO_STAGE
+    const uint32_t stage_bytes = 2 * buf_bytes;
+#else
+    const uint32_t stage_bytes = 512;  // L1-warming scratch: 16 B per lane
+#endif
+    uint32_t* vis = reinterpret_cast<uint32_t*>(smem_raw + stage_bytes);
+    const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+    const uint32_t* wrow = BUF ? a.words + (a.force ? 0 : (uint64_t)ant * a.stride) : nullptr;
     auto word = [&](uint32_t slot) -> uint32_t {
-        if (a.words) return a.words[(a.force ? 0 : (uint64_t)ant * a.stride) + slot];
-        const uint4 v = philox10(make_uint4(slot >> 2, ant, (uint32_t)a.iter, (uint32_t)(a.iter >> 32)),
-                                 make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32)));
+        if (BUF) return wrow[slot];
+        const uint4 v = philox10(make_uint4(slot >> 2, ant, (uint32_t)a.iter, (uint32_t)(a.iter >> 32)), key);
         return pick_word(v, slot & 3);
     };
     for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
@@ -439,77 +498,166 @@ __global__ void __launch_bounds__(32) k_construct(ConstructArgs a) {
     }
     __syncwarp();
 
-    unsigned long long n_dec = 0, n_fb = 0, n_tie = 0, n_forced = 0;
-    uint4 pw = make_uint4(0, 0, 0, 0);
-    const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+    uint32_t n_dec = 0, n_fb = 0, n_tie = 0, n_forced = 0;
+    uint4 pb = make_uint4(0, 0, 0, 0);  // Philox block of this lane for the current 128-decision batch
     uint32_t remaining = n - pos;
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t vis_s = stage_s + stage_bytes;
+    const uint32_t warm_s = stage_s;
+    // lanes >= k never load: they hold (cur, 0.0f), and cur is always marked visited
+    const bool lane_in = lane < k;
+    const uint2* __restrict__ row_base = a.cand + lane;
+    const uint32_t iter_lo = (uint32_t)a.iter, iter_hi = (uint32_t)(a.iter >> 32);
+    FbStats fs;
+    uint32_t stage_row = 0xffffffffu;  // shared address of cur's staged row (this lane's entry), or none
+    uint32_t sbuf = 0;
+#ifdef PACO_TIMING
+    const long long loop0 = clock64();
+    long long seg0 = 0, seg1 = 0, seg2 = 0, segn = 0, fbc = 0, segw = 0, sege = 0;
+#endif
+    uint32_t uw = 0;  // draw word of the current decision (slot 4 + t)
+    // candidate row entry of the current decision
+    uint2 e_pre = ldg_u64_if(row_base + (size_t)cur * kp, lane_in && remaining > 1, make_uint2(cur, 0u));
+    if (!BUF) {
+        pb = philox10(make_uint4(1 + lane, ant, iter_lo, iter_hi), key);
+        uw = __shfl_sync(kFull, pb.x, 0);
+    } else if (remaining > 1) {
+        uw = wrow[4];
+    }
     for (uint32_t t = 0; remaining > 0; ++t, --remaining) {
         uint32_t next;
         ++n_dec;
-        if (remaining == 1) {
-            next = last_unvisited(vis, nw, lane);
-            ++n_forced;
-#ifdef PACO_DEBUG
-            {
-                uint32_t zeros = 0;
-                for (uint32_t w = lane; w < nw; w += 32) zeros += __popc(~vis[w]);
-                for (int off = 16; off; off >>= 1) zeros += __shfl_xor_sync(kFull, zeros, off);
-                if (lane == 0 && zeros != 1) printf("DBG ant %u pos %u forced: zeros=%u next=%u\n", ant, pos, zeros, next);
-            }
+        if (remaining > 1) {
+            PACO_CLOCK(ta, t);
+            // 1. head of the dependent chain: cur's candidate row, on chip when the previous
+            //    decision staged it, else from L2
+#ifdef PACO_STAGE
+            uint2 e = make_uint2(cur, 0u);
+            cp_async_wait_all();
+            __syncwarp();
+            PACO_CLOCK(tw, t);
+            if (stage_row != 0xffffffffu) { if (lane_in) e = lds_u64(stage_row); }
+            else if (lane_in) e = ldg_u64(row_base + (size_t)cur * kp);
+#else
+            __syncwarp();
+            PACO_CLOCK(tw, t);
+            const uint2 e = e_pre;  // issued at the end of the previous decision
 #endif
-        } else {
-            uint32_t uw;
-            if (a.words) uw = a.words[(a.force ? 0 : (uint64_t)ant * a.stride) + 4 + t];
-            else {
-                if ((t & 3) == 0)
-                    pw = philox10(make_uint4(1 + (t >> 2), ant, (uint32_t)a.iter, (uint32_t)(a.iter >> 32)), key);
-                uw = pick_word(pw, t & 3);
-            }
-            uint2 e = make_uint2(kNone, 0u);
-            if (lane < k) e = __ldg(&a.cand[(size_t)cur * k + lane]);
-            float w = 0.0f;
-            if (lane < k && !is_visited(vis, e.x)) w = __uint_as_float(e.y);
-            // Hillis-Steele inclusive scan over the k candidate lanes
+            PACO_CLOCK(te, e.x);
+            // 2. feasibility from the bitmap
+            const uint32_t vw = lds_u32(vis_s + ((e.x >> 5) << 2));
+            const float w = ((vw >> (e.x & 31)) & 1u) ? 0.0f : __uint_as_float(e.y);
+            PACO_CLOCK(tb, __float_as_uint(w));
+            // 3. Hillis-Steele inclusive scan over the candidate lanes; the staging copies of
+            //    the feasible candidates' rows issue in the shadow of the first shuffle
             float v = w;
-            for (uint32_t off = 1; off < k; off <<= 1) {
-                const float y = __shfl_up_sync(kFull, v, off);
-                if (lane >= off) v = __fadd_rn(v, y);
+            {
+                const float y = __shfl_up_sync(kFull, v, 1u);
+#ifndef PACO_STAGE
+                // warm L1 with every feasible candidate's row: an LDGSTS (cp.async.ca) per 32-byte
+                // sector into a per-lane scratch slot that is never read. On B200 this is what
+                // makes the next decision's row load an L1 hit: prefetch.global.L1 measured no
+                // effect (scratch microbenchmark, profiles/README.md).
+                {
+                    const bool cp = w > 0.0f;
+                    const unsigned char* src = reinterpret_cast<const unsigned char*>(a.cand + (size_t)e.x * kp);
+                    const uint32_t dst = warm_s + lane * 16;
+                    if (KP) {
+#pragma unroll
+                        for (int c = 0; c < (KP * 8 + 31) / 32; ++c) cp_async16_if(dst, src + 32 * c, cp);
+                    } else {
+                        for (uint32_t c = 0; c < (kp * 8 + 31) / 32; ++c) cp_async16_if(dst, src + 32 * c, cp);
+                    }
+                }
+#endif
+#ifdef PACO_STAGE
+                sbuf ^= 1u;
+                const bool cp = w > 0.0f;
+                const unsigned char* src = reinterpret_cast<const unsigned char*>(a.cand + (size_t)e.x * kp);
+                const uint32_t dst = stage_s + sbuf * buf_bytes + lane * slot_bytes;
+                if (KP) {
+#pragma unroll
+                    for (int c = 0; c < KP / 2; ++c) cp_async16_if(dst + 16 * c, src + 16 * c, cp);
+                } else {
+                    for (uint32_t c = 0; c < kp / 2; ++c) cp_async16_if(dst + 16 * c, src + 16 * c, cp);
+                }
+                cp_async_commit();
+#endif
+                if (lane >= 1u) v = __fadd_rn(v, y);
             }
+#pragma unroll
+            for (int st = 1; st < STEPS; ++st) {
+                const float y = __shfl_up_sync(kFull, v, 1u << st);
+                if (lane >= (1u << st)) v = __fadd_rn(v, y);
+            }
+            const float u = u01_f32(uw);
             const float S = __shfl_sync(kFull, v, k - 1);
+            PACO_CLOCK(tc, __float_as_uint(S));
             if (S > 0.0f) {
-                const float target = __fmul_rn(u01_f32(uw), S);
+                const float target = __fmul_rn(u, S);
                 const float tol = __fmul_rn(1e-6f, S);
-                const bool in = lane < k;
-                if (__any_sync(kFull, in && fabsf(__fsub_rn(v, target)) <= tol)) ++n_tie;
-                // only feasible lanes may win: the tree-shaped scan is not monotone in f32,
-                // so an infeasible lane's S_r can exceed its left neighbour's by an ulp
-                unsigned ball = __ballot_sync(kFull, in && w > 0.0f && v > target);
-                int r;
-                if (ball) r = __ffs(ball) - 1;
-                else r = 31 - __clz(__ballot_sync(kFull, in && w > 0.0f));
+                // only feasible lanes (w > 0; lanes >= k have w = 0) may win: the tree-shaped
+                // scan is not monotone in f32, so an infeasible lane's S_r can exceed its left
+                // neighbour's by an ulp. The three votes are independent and issue together.
+                const unsigned ball = __ballot_sync(kFull, w > 0.0f && v > target);
+                const unsigned feas = __ballot_sync(kFull, w > 0.0f);
+                const unsigned tie = __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(v, target)) <= tol);
+                const int r = ball ? __ffs(ball) - 1 : 31 - __clz(feas);
                 next = __shfl_sync(kFull, e.x, r);
+                stage_row = stage_s + sbuf * buf_bytes + (uint32_t)r * slot_bytes + lane * 8;
+                n_tie += tie ? 1u : 0u;
+                PACO_CLOCK(td, next);
+#ifdef PACO_TIMING
+                seg0 += tb - ta; seg1 += tc - tb; seg2 += td - tc; ++segn; segw += tw - ta; sege += te - tw; if (lane == 0 && stage_row == 0xffffffffu) {}
+#endif
             } else {
-                next = nearest_unvisited(a, vis, cur, lane);
+#ifdef PACO_TIMING
+                const long long c0 = clock64();
+#endif
+                next = nearest_unvisited(a, vis, cur, lane, fs);
+#ifdef PACO_TIMING
+                fbc += clock64() - c0;
+#endif
+                stage_row = 0xffffffffu;
                 ++n_fb;
             }
+        } else {
+            __syncwarp();
+            next = last_unvisited(vis, nw, lane);
+            ++n_forced;
         }
-#ifdef PACO_DEBUG
-        {
-            const uint32_t nx0 = __shfl_sync(kFull, next, 0);
-            if (!__all_sync(kFull, nx0 == next) && lane == 0) printf("DBG ant %u pos %u non-uniform next\n", ant, pos);
-            if (is_visited(vis, next)) {
-                for (uint32_t q = lane; q < pos; q += 32)
-                    if (out[q] == next) printf("DBG ant %u pos %u dup next=%u rem=%u earlier at %u (partial=%d start_pos=%u m_mod=%u)\n", ant, pos, next, remaining, q, (int)partial, start_pos, m_mod);
-                if (lane == 0) printf("DBG ant %u pos %u dup next=%u word=%08x\n", ant, pos, next, vis[next >> 5]);
-            }
-        }
+        // off-chain bookkeeping after the pick, overlapping the loop turn: the visit of next
+        // (one lane, fire-and-forget; the __syncwarp at the top of the next decision orders
+        // it for every lane, and no candidate of next is next itself), the tour entry and
+        // the next decision's draw word
+#ifndef PACO_STAGE
+        // head of the next decision's dependent chain, issued before any bookkeeping
+        e_pre = ldg_u64_if(row_base + (size_t)next * kp, lane_in, make_uint2(next, 0u));
 #endif
-        if (lane == 0) { out[pos] = next; vis[next >> 5] |= 1u << (next & 31); }
-        __syncwarp();
+        red_or_shared_if(vis_s + ((next >> 5) << 2), 1u << (next & 31), lane == 0);
+        stg_u32_if(out + pos, next, lane == 0);
         ++pos;
         cur = next;
+        if (!BUF) {
+            const uint32_t t1 = t + 1;
+            if ((t1 & 127) == 0) pb = philox10(make_uint4(1 + (t1 >> 2) + lane, ant, iter_lo, iter_hi), key);
+            uw = __shfl_sync(kFull, pick_word(pb, t1 & 3), (t1 & 127) >> 2);
+        } else if (remaining > 2) {
+            uw = wrow[4 + t + 1];
+        }
     }
+    cp_async_wait_all();
     __syncwarp();
+#ifdef PACO_TIMING
+    if (lane == 0) { atomicAdd(&g_timing[0], (unsigned long long)(clock64() - loop0)); atomicAdd(&g_timing[2], (unsigned long long)n_dec);
+        atomicAdd(&g_timing[1], (unsigned long long)fbc);
+        atomicAdd(&g_timing[4], (unsigned long long)seg0); atomicAdd(&g_timing[5], (unsigned long long)seg1);
+        atomicAdd(&g_timing[6], (unsigned long long)seg2); atomicAdd(&g_timing[7], (unsigned long long)segn);
+        atomicAdd(&g_timing[3], (unsigned long long)segw); atomicAdd(&g_timing[8], (unsigned long long)sege); }
+    { long long c = fs.cities; for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+      if (lane == 0) { atomicAdd(&g_timing[9], (unsigned long long)fs.searches); atomicAdd(&g_timing[10], (unsigned long long)fs.rings);
+        atomicAdd(&g_timing[11], (unsigned long long)fs.sbs); atomicAdd(&g_timing[12], (unsigned long long)c); } }
+#endif
     // tour length (instance.hpp:120-127), int64, warp-parallel over positions
     long long len = 0;
     for (uint32_t p = lane; p < n; p += 32) {
@@ -535,10 +683,10 @@ __global__ void __launch_bounds__(32) k_construct(ConstructArgs a) {
         a.new_len[ant] = len;
         if (!a.force) {
             a.partial_flag[ant] = partial ? 1 : 0;
-            atomicAdd(&a.counters[0], n_dec);
-            atomicAdd(&a.counters[1], n_fb);
-            atomicAdd(&a.counters[2], n_tie);
-            atomicAdd(&a.counters[3], n_forced);
+            atomicAdd(&a.counters[0], (unsigned long long)n_dec);
+            atomicAdd(&a.counters[1], (unsigned long long)n_fb);
+            atomicAdd(&a.counters[2], (unsigned long long)n_tie);
+            atomicAdd(&a.counters[3], (unsigned long long)n_forced);
             atomicAdd(&a.counters[partial ? 5 : 4], 1ull);
         }
     }
@@ -592,7 +740,7 @@ __global__ void k_publish(const uint32_t* __restrict__ tours, const uint8_t* __r
 // T = max(T (1-rho), 1e-6), then for every built tour in tour order T += 1/C_a when
 // the tour contains the edge. cur_nbr holds the built tours' neighbour pairs.
 template <int KMAX>
-__global__ void __launch_bounds__(256) k_classic(const uint32_t* __restrict__ knn, const uint2* __restrict__ cur_nbr,
+__global__ void __launch_bounds__(256) k_classic(const uint32_t* __restrict__ knn32, const uint2* __restrict__ cur_nbr,
                                                  const int64_t* __restrict__ new_len, uint32_t n, uint32_t m, int k,
                                                  double rho, double* __restrict__ T) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -602,7 +750,7 @@ __global__ void __launch_bounds__(256) k_classic(const uint32_t* __restrict__ kn
     const double keep = 1.0 - rho;
 #pragma unroll
     for (int r = 0; r < KMAX; ++r) {
-        c[r] = r < k ? knn[(size_t)i * k + r] : kNone;
+        c[r] = r < k ? knn32[(size_t)i * 32 + r] : kNone;
         if (r < k) {
             double v = __dmul_rn(T[(size_t)i * k + r], keep);
             t[r] = v < 1e-6 ? 1e-6 : v;

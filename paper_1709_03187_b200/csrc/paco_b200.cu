@@ -51,7 +51,7 @@ struct paco_handle {
     cudaStream_t st = nullptr;
     paco_config cfg{};
     int mode = 0;
-    uint32_t n = 0, m = 0, k = 0, nwords = 0;
+    uint32_t n = 0, m = 0, k = 0, kp = 0, nwords = 0;
     GridParams g{};
     std::vector<double> hx, hy;
     std::vector<uint32_t> h_orig, h_int;
@@ -178,7 +178,8 @@ static paco_status setup(paco_handle* h) {
     CU(dalloc(&keys, n)); CU(dalloc(&keys2, n)); CU(dalloc(&cellm, n));
     CU(dalloc(&h->xy, n)); CU(dalloc(&h->orig_of, n)); CU(dalloc(&h->int_of, n));
     CU(dalloc(&h->cell_start, (size_t)h->g.ncells + 1));
-    CU(dalloc(&h->knn, (size_t)n * k)); CU(dalloc(&h->eta, (size_t)n * k)); CU(dalloc(&h->cand, (size_t)n * k));
+    CU(dalloc(&h->knn, (size_t)n * 32)); CU(dalloc(&h->eta, (size_t)n * k)); CU(dalloc(&h->cand, (size_t)n * h->kp));
+    CU(cudaMemsetAsync(h->cand, 0, sizeof(uint2) * (size_t)n * h->kp, st));
     CU(dalloc(&h->tours, (size_t)m * 2 * n));
     CU(dalloc(&h->lb_sel, m)); CU(dalloc(&h->has_lb, m)); CU(dalloc(&h->improved, m)); CU(dalloc(&h->partial, m));
     CU(dalloc(&h->new_len, m)); CU(dalloc(&h->lb_len, m)); CU(dalloc(&h->g_len, 1));
@@ -227,15 +228,10 @@ static paco_status setup(paco_handle* h) {
     const uint32_t nsb = h->g.ncells >> 6;
     uint32_t* nglob = h->scratch_u32;
     CU(cudaMemsetAsync(nglob, 0, sizeof(uint32_t), st));
-    const int km = kmax_for(k);
-#define LAUNCH_KNN(KM)                                                                                  \
-    do {                                                                                                \
-        CU(cudaFuncSetAttribute(k_knn<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
-        k_knn<KM><<<nsb, 128, smem, st>>>(h->xy, h->orig_of, h->cell_start, h->g, n, (int)k,            \
-                                          h->cfg.beta, cap, h->knn, h->eta, nglob);                     \
-    } while (0)
-    if (km == 8) LAUNCH_KNN(8); else if (km == 16) LAUNCH_KNN(16); else if (km == 24) LAUNCH_KNN(24); else LAUNCH_KNN(32);
-#undef LAUNCH_KNN
+    const int kk = (int)std::min<uint32_t>(32, n - 1);
+    CU(cudaFuncSetAttribute(k_knn<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_knn<32><<<nsb, 128, smem, st>>>(h->xy, h->orig_of, h->cell_start, h->g, n, kk, (int)k, h->cfg.beta, cap,
+                                      h->knn, h->eta, nglob);
     CU(cudaGetLastError());
     CU(cudaEventRecord(e1, st));
     CU(cudaStreamSynchronize(st));
@@ -270,7 +266,8 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
     CU(cudaGetDeviceProperties(&prop, dev));
     if (prop.major != 10) return fail(PACO_E_CUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
     const uint32_t nwords = (n + 31) / 32;
-    if ((size_t)nwords * 4 > (size_t)prop.sharedMemPerBlockOptin)
+    const uint32_t kk = std::min<uint32_t>(cfg->candidates, n - 1), kpp = (kk + 1) & ~1u;
+    if ((size_t)nwords * 4 + (size_t)2 * kk * kpp * 8 > (size_t)prop.sharedMemPerBlockOptin)
         return fail(PACO_E_UNSUPPORTED, "visited bitmap exceeds shared memory (n too large)");
     auto* h = new (std::nothrow) paco_handle();
     if (!h) return fail(PACO_E_RUNTIME, "out of host memory");
@@ -278,6 +275,7 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
     h->cfg = *cfg;
     h->mode = mode;
     h->n = n; h->m = cfg->ants; h->k = std::min<uint32_t>(cfg->candidates, n - 1); h->nwords = nwords;
+    h->kp = (h->k + 1) & ~1u;
     h->hx.assign(xs, xs + n); h->hy.assign(ys, ys + n);
     if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
         delete h;
@@ -310,7 +308,7 @@ static paco_status launch_weights(paco_handle* h) {
         if (smem > 48 * 1024)                                                                              \
             CU(cudaFuncSetAttribute(k_weights<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
         k_weights<KM><<<(n + tb - 1) / tb, tb, smem, h->st>>>(h->knn, h->eta, h->nbr, h->lb_len, h->has_lb,  \
-                                                            h->g_len, T, n, h->m, (int)h->k, h->cfg.alpha, \
+                                                            h->g_len, T, n, h->m, (int)h->k, (int)h->kp, h->cfg.alpha, \
                                                             h->cfg.tau0, h->cand);                         \
     } while (0)
     if (km == 8) LAUNCH_W(8); else if (km == 16) LAUNCH_W(16); else if (km == 24) LAUNCH_W(24); else LAUNCH_W(32);
@@ -321,12 +319,12 @@ static paco_status launch_weights(paco_handle* h) {
 
 static ConstructArgs construct_args(paco_handle* h, bool seeding) {
     ConstructArgs a{};
-    a.cand = h->cand; a.xy = h->xy; a.orig_of = h->orig_of; a.int_of = h->int_of;
+    a.cand = h->cand; a.knn32 = h->knn; a.xy = h->xy; a.orig_of = h->orig_of; a.int_of = h->int_of;
     a.cell_start = h->cell_start; a.g = h->g; a.tours = h->tours; a.lb_sel = h->lb_sel;
     a.new_len = h->new_len; a.partial_flag = h->partial; a.counters = h->counters;
     a.words = h->cfg.draws == PACO_DRAWS_BUFFER ? h->words : nullptr;
     a.stride = h->words_stride; a.seed = h->cfg.seed; a.iter = h->iter;
-    a.n = h->n; a.m = h->m; a.k = h->k; a.nwords = h->nwords;
+    a.n = h->n; a.m = h->m; a.k = h->k; a.kp = h->kp; a.nwords = h->nwords;
     a.eff_pp = h->mode == PACO_MODE_PARTIAL ? h->cfg.partial_prob : 0.0;  // engine.hpp:164-165
     a.mmf = h->cfg.max_mod_frac;
     a.seeding = seeding ? 1 : 0;
@@ -336,12 +334,24 @@ static ConstructArgs construct_args(paco_handle* h, bool seeding) {
 }
 
 static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint32_t blocks) {
-    const size_t smem = (size_t)h->nwords * 4;
-    if (smem > 48 * 1024)
-        CU(cudaFuncSetAttribute(k_construct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_construct<<<blocks, 32, smem, h->st>>>(a);
-    CU(cudaGetLastError());
-    return PACO_OK;
+    // shared memory: double-buffered stage of k candidate rows + the n-bit visited bitmap
+#ifdef PACO_STAGE
+    const size_t smem = (size_t)2 * h->k * h->kp * 8 + (size_t)h->nwords * 4;
+#else
+    const size_t smem = 512 + (size_t)h->nwords * 4;
+#endif
+    const bool buf = a.words != nullptr;
+    auto launch = [&](auto kern) -> paco_status {
+        if (smem > 48 * 1024)
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<blocks, 32, smem, h->st>>>(a);
+        CU(cudaGetLastError());
+        return PACO_OK;
+    };
+    if (h->kp == 16) return buf ? launch(k_construct<16, 4, true>) : launch(k_construct<16, 4, false>);
+    if (h->kp == 20) return buf ? launch(k_construct<20, 5, true>) : launch(k_construct<20, 5, false>);
+    // generic k: runtime row stride, five scan steps (extra steps never touch lanes < k)
+    return buf ? launch(k_construct<0, 5, true>) : launch(k_construct<0, 5, false>);
 }
 
 static paco_status check_err(paco_handle* h) {
@@ -508,19 +518,26 @@ paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, u
     CU(cudaSetDevice(h->dev));
     const uint32_t n = h->n, k = h->k;
     if (k_out) *k_out = k;
-    std::vector<uint2> c((size_t)n * k);
-    std::vector<uint32_t> kn((size_t)n * k);
+    std::vector<uint2> c((size_t)n * h->kp);
+    std::vector<uint32_t> kn((size_t)n * 32);
     CU(cudaMemcpy(kn.data(), h->knn, sizeof(uint32_t) * kn.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(c.data(), h->cand, sizeof(uint2) * c.size(), cudaMemcpyDeviceToHost));
     for (uint32_t o = 0; o < n; ++o) {
         const uint32_t i = h->h_int[o];
         for (uint32_t r = 0; r < k; ++r) {
-            if (knn) knn[(size_t)o * k + r] = h->h_orig[kn[(size_t)i * k + r]];
-            if (weights) std::memcpy(&weights[(size_t)o * k + r], &c[(size_t)i * k + r].y, 4);
+            if (knn) knn[(size_t)o * k + r] = h->h_orig[kn[(size_t)i * 32 + r]];
+            if (weights) std::memcpy(&weights[(size_t)o * k + r], &c[(size_t)i * h->kp + r].y, 4);
         }
     }
     return PACO_OK;
 }
+
+#ifdef PACO_TIMING
+extern "C" void paco_debug_timing(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_timing, sizeof(unsigned long long) * 16);
+    if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_timing, z, sizeof z); }
+}
+#endif
 
 paco_status paco_get_timing(paco_handle* h, double* c, double* u, double* s) {
     if (!h) return fail(PACO_E_INVALID, "null handle");
