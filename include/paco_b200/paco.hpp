@@ -1,0 +1,188 @@
+// paco_b200/paco.hpp -- C++ drop-in for the reference solver interface.
+//
+// Mirrors /root/reference/proj/include/paco/engine.hpp (Mode :24, mode_name /
+// mode_from_name :26-40, RunConfig :42-76, ConvergenceSample :78-82, RunReport
+// :84-92, run :156, run_timed_baseline :339-344) and the Instance / Tour types
+// of instance.hpp:41-107, so a caller of paco::run can switch namespaces:
+//
+//     #include "paco_b200/paco.hpp"
+//     auto report = paco_b200::run(inst, cfg, paco_b200::Mode::partial_aco);
+//
+// Everything below is a thin header-only layer over the C ABI in paco_b200.h
+// (link with -lpaco_b200); status codes are rethrown as the reference's
+// exception types (std::invalid_argument, std::logic_error, std::runtime_error).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../paco_b200.h"
+
+namespace paco_b200 {
+
+enum class Mode { partial_aco, paco_full, classic_aco };
+
+inline const char* mode_name(Mode m) {
+    switch (m) {
+        case Mode::partial_aco: return "partial";
+        case Mode::paco_full: return "paco";
+        case Mode::classic_aco: return "classic";
+    }
+    return "?";
+}
+
+inline std::optional<Mode> mode_from_name(const std::string& s) {
+    if (s == "partial") return Mode::partial_aco;
+    if (s == "paco") return Mode::paco_full;
+    if (s == "classic") return Mode::classic_aco;
+    return std::nullopt;
+}
+
+inline void check(paco_status s) {
+    if (s == PACO_OK) return;
+    const std::string msg = paco_last_error();
+    if (s == PACO_E_INVALID) throw std::invalid_argument(msg);
+    if (s == PACO_E_LOGIC) throw std::logic_error(msg);
+    throw std::runtime_error(msg);
+}
+
+// RunConfig, engine.hpp:42-76 (same fields and defaults) + the north-star knob.
+struct RunConfig {
+    std::uint32_t ants = 16;
+    std::uint64_t iterations = 100000;
+    double alpha = 5.0;
+    double beta = 5.0;
+    double partial_prob = 0.95;
+    double max_mod_frac = 1.0;
+    double two_opt_prob = 0.0;
+    std::uint32_t two_opt_window = 0;
+    std::uint32_t workers = 8;
+    std::uint64_t seed = 1;
+    double rho = 0.1;
+    double tau_max = 1.0;
+    double tau0 = 1.0;
+    double time_budget_s = 0.0;
+    double convergence_interval_s = 1.0;
+    bool synchronous = true;  // the GPU engine runs barrier-synchronous iterations
+    bool validate_tours = false;
+    std::uint32_t candidates = 16;  // k of the k-NN candidate list
+    int device = -1;
+
+    paco_config to_c() const {
+        paco_config c{};
+        check(paco_config_default(&c));
+        c.ants = ants; c.iterations = iterations; c.alpha = alpha; c.beta = beta;
+        c.partial_prob = partial_prob; c.max_mod_frac = max_mod_frac; c.two_opt_prob = two_opt_prob;
+        c.two_opt_window = two_opt_window; c.workers = workers; c.seed = seed; c.rho = rho;
+        c.tau_max = tau_max; c.tau0 = tau0; c.time_budget_s = time_budget_s;
+        c.convergence_interval_s = convergence_interval_s; c.synchronous = synchronous ? 1u : 0u;
+        c.validate_tours = validate_tours ? 1u : 0u; c.candidates = candidates;
+        c.draws = PACO_DRAWS_PHILOX; c.device = device;
+        return c;
+    }
+
+    // RunConfig::validate (engine.hpp:61-75)
+    void validate() const {
+        const paco_config c = to_c();
+        check(paco_config_validate(&c, 3, 0));
+    }
+};
+
+struct Tour {
+    std::vector<std::uint32_t> order;
+    std::int64_t length = 0;
+};
+
+// Immutable city set (instance.hpp:41-101): coordinates plus EUC_2D.
+class Instance {
+public:
+    Instance(std::string name, std::vector<std::pair<double, double>> coords,
+             std::optional<std::int64_t> optimum = std::nullopt)
+        : name_(std::move(name)), optimum_(optimum) {
+        if (coords.size() < 3)
+            throw std::invalid_argument("instance needs at least 3 cities, got " + std::to_string(coords.size()));
+        if (optimum_ && *optimum_ <= 0) throw std::invalid_argument("known optimum must be positive");
+        xs_.reserve(coords.size());
+        ys_.reserve(coords.size());
+        for (const auto& [x, y] : coords) {
+            if (!std::isfinite(x) || !std::isfinite(y)) throw std::invalid_argument("non-finite coordinate");
+            xs_.push_back(x);
+            ys_.push_back(y);
+        }
+    }
+    const std::string& name() const { return name_; }
+    std::uint32_t n() const { return static_cast<std::uint32_t>(xs_.size()); }
+    double x(std::uint32_t i) const { return xs_[i]; }
+    double y(std::uint32_t i) const { return ys_[i]; }
+    const double* xs() const { return xs_.data(); }
+    const double* ys() const { return ys_.data(); }
+    std::optional<std::int64_t> optimum() const { return optimum_; }
+    std::int32_t dist(std::uint32_t i, std::uint32_t j) const {  // instance.hpp:33-37
+        const double dx = xs_[i] - xs_[j], dy = ys_[i] - ys_[j];
+        return static_cast<std::int32_t>(std::sqrt(dx * dx + dy * dy) + 0.5);
+    }
+
+private:
+    std::string name_;
+    std::vector<double> xs_, ys_;
+    std::optional<std::int64_t> optimum_;
+};
+
+struct ConvergenceSample {
+    double elapsed_s;
+    std::int64_t g_best_length;
+    std::uint64_t iterations_done;
+};
+
+// RunReport, engine.hpp:84-92, plus the engine's counters and device timings.
+struct RunReport {
+    std::int64_t best_length = 0;
+    Tour best_tour;
+    std::optional<double> pct_error;
+    double wall_time_s = 0.0;
+    std::uint64_t iterations_done = 0;
+    std::uint64_t comparisons_total = 0;
+    std::vector<ConvergenceSample> convergence;
+    paco_counters counters{};
+    double construct_ms = 0.0, update_ms = 0.0, setup_ms = 0.0;
+};
+
+inline paco_mode to_c(Mode m) {
+    return m == Mode::partial_aco ? PACO_MODE_PARTIAL : m == Mode::paco_full ? PACO_MODE_PACO : PACO_MODE_CLASSIC;
+}
+
+// paco::run (engine.hpp:156-333) on the B200 engine.
+inline RunReport run(const Instance& inst, const RunConfig& cfg, Mode mode) {
+    const paco_config c = cfg.to_c();
+    paco_report rep{};
+    RunReport out;
+    out.best_tour.order.resize(inst.n());
+    check(paco_run(inst.xs(), inst.ys(), inst.n(), &c, to_c(mode), inst.optimum().value_or(0), &rep,
+                   out.best_tour.order.data()));
+    out.best_length = rep.best_length;
+    out.best_tour.length = rep.best_length;
+    if (inst.optimum()) out.pct_error = rep.pct_error;
+    out.wall_time_s = rep.wall_time_s;
+    out.iterations_done = rep.iterations_done;
+    out.comparisons_total = rep.comparisons_total;
+    out.counters = rep.counters;
+    out.construct_ms = rep.construct_ms;
+    out.update_ms = rep.update_ms;
+    out.setup_ms = rep.setup_ms;
+    out.convergence.push_back({out.wall_time_s, out.best_length, out.iterations_done});
+    return out;
+}
+
+// engine.hpp:339-344
+inline RunReport run_timed_baseline(const Instance& inst, RunConfig cfg, double budget_s) {
+    if (budget_s <= 0.0) throw std::invalid_argument("budget must be positive");
+    cfg.time_budget_s = budget_s;
+    return run(inst, cfg, Mode::paco_full);
+}
+
+}  // namespace paco_b200

@@ -1,0 +1,124 @@
+#!/usr/bin/env python
+"""Generate tests/golden/ref_golden.npz from the UNMODIFIED reference (O1).
+
+Test infrastructure. Runs only in a container where /root/reference exists: it
+builds oracle/_ref/libpaco_ref.so from the reference headers (oracle/Makefile)
+and records the reference's own outputs for the pieces of the hot path that the
+O2 restatement and the GPU engine must reproduce. The fixtures travel with the
+repo, so the pinning tests run anywhere (including the GPU box, which has no
+/root/reference).
+
+    python oracle/make_golden.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, HERE)
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden", "ref_golden.npz")
+
+
+def main() -> None:
+    oracle.build(ref=True)
+    rng = np.random.default_rng(20240917)
+    L = oracle.reflib()
+    g = {}
+
+    # --- EUC_2D (instance.hpp:33-37): test_instance.cpp:136-145 points + random pairs
+    kat = np.array([[0, 0, 3, 4], [0, 0, 1, 1], [0, 0, 0.5, 0], [0, 0, 10, 0], [0, 0, 0, 0]], dtype=np.float64)
+    rnd_i = rng.integers(0, 10_000_000, size=(2000, 4)).astype(np.float64)
+    rnd_f = rng.random((2000, 4)) * 1000.0
+    pts = np.concatenate([kat, rnd_i, rnd_f])
+    g["euc2d_pts"] = pts
+    g["euc2d_ref"] = np.array([L.ref_euc2d(*p) for p in pts], dtype=np.int32)
+
+    # --- Power (construction.hpp:19-44)
+    es = np.array([0, 1, 2, 3, 5, 7, 64, 2.5, 0.5], dtype=np.float64)
+    xs = np.array([1e-7, 0.5, 1.0, 2.0, 3.0, 123.4], dtype=np.float64)
+    pe = np.array([(e, x) for e in es for x in xs], dtype=np.float64)
+    g["power_args"] = pe
+    g["power_ref"] = np.array([L.ref_power(e, x) for e, x in pe], dtype=np.float64)
+
+    # --- tau^alpha through Colony + ColonyPheromone (colony.hpp:115-177, construction.hpp:104-158)
+    cases = []
+    for ci, (n, m, alpha) in enumerate([(10, 3, 1.0), (20, 5, 2.0), (37, 8, 5.0), (50, 16, 1.0), (12, 4, 0.0)]):
+        x = rng.integers(0, 1000, n).astype(np.float64)
+        y = rng.integers(0, 1000, n).astype(np.float64)
+        tours = np.stack([rng.permutation(n) for _ in range(m)]).astype(np.uint32)
+        if ci == 1:
+            tours[3] = tours[1]  # equal lengths: the incumbent keeps g_best
+        tau, direct, glen = oracle.ref_colony_tau(x, y, tours, 1.0, alpha, direct=True)
+        g[f"tau{ci}_x"], g[f"tau{ci}_y"], g[f"tau{ci}_tours"] = x, y, tours
+        g[f"tau{ci}_alpha"] = np.float64(alpha)
+        g[f"tau{ci}_ref"] = tau
+        g[f"tau{ci}_direct"] = direct
+        g[f"tau{ci}_glen"] = np.int64(glen)
+        cases.append(ci)
+    g["tau_cases"] = np.array(cases)
+
+    # --- eta^beta (Heuristic, construction.hpp:49-82), table path and on-the-fly path
+    for tag, n in (("table", 200), ("fly", 5001)):
+        x = rng.integers(0, 100_000, n).astype(np.float64)
+        y = rng.integers(0, 100_000, n).astype(np.float64)
+        x[5], y[5] = x[6], y[6]  # a duplicate point: d = 0 -> clamp to 1
+        pairs = np.stack([rng.integers(0, n, 400), rng.integers(0, n, 400)], axis=1).astype(np.uint32)
+        pairs[0] = (5, 6)
+        pairs = pairs[pairs[:, 0] != pairs[:, 1]]
+        for beta in (2.0, 5.0):
+            g[f"eta_{tag}_b{int(beta)}_ref"] = oracle.ref_eta_beta(x, y, beta, pairs)
+        g[f"eta_{tag}_x"], g[f"eta_{tag}_y"], g[f"eta_{tag}_pairs"] = x, y, pairs
+
+    # --- completion-step update semantics (colony.hpp:115-139, engine.hpp:261-265)
+    n, m = 9, 4
+    x = rng.integers(0, 50, n).astype(np.float64)
+    y = rng.integers(0, 50, n).astype(np.float64)
+    count = 60
+    tours = np.stack([rng.permutation(n) for _ in range(count)]).astype(np.uint32)
+    tours[10] = tours[3]  # exact repeats -> ties
+    tours[20] = np.roll(tours[7], 3)  # rotation -> equal length
+    ants = rng.integers(0, m, count).astype(np.uint32)
+    flags, gafter = oracle.ref_offer_sequence(x, y, m, tours, ants)
+    g.update(offer_x=x, offer_y=y, offer_tours=tours, offer_ants=ants, offer_flags=flags, offer_g=gafter)
+
+    # --- classic evaporate/deposit (construction.hpp:160-213)
+    n = 12
+    rounds, ntours = 3, 4
+    ct = np.stack([[rng.permutation(n) for _ in range(ntours)] for _ in range(rounds)]).astype(np.uint32)
+    cl = rng.integers(50, 200, size=(rounds, ntours)).astype(np.int64)
+    g.update(classic_tours=ct, classic_lens=cl, classic_rho=np.float64(0.5), classic_tau=np.float64(1.0))
+    g["classic_ref"] = oracle.ref_classic_update(n, 0.5, 1.0, ct, cl)
+
+    # --- Rng::for_stream (rng.hpp:33-50) raw outputs, for the IR-rule mode
+    g["stream_ref"] = np.stack([oracle.ref_stream_u64(7, s, 64) for s in range(4)])
+
+    # --- whole-run reference results (IR rule, sync mode) on small instances
+    runs = []
+    for ri, (n, m, iters, mode) in enumerate([(12, 4, 30, "partial"), (30, 8, 20, "paco"), (25, 6, 10, "classic")]):
+        x = rng.integers(0, 1000, n).astype(np.float64)
+        y = rng.integers(0, 1000, n).astype(np.float64)
+        r = oracle.ref_run(x, y, ants=m, iterations=iters, alpha=1.0, beta=2.0, seed=11 + ri, mode=mode,
+                           workers=2, rho=0.5)
+        g[f"run{ri}_x"], g[f"run{ri}_y"] = x, y
+        g[f"run{ri}_cfg"] = np.array([n, m, iters, ["partial", "paco", "classic"].index(mode), 11 + ri])
+        g[f"run{ri}_best"] = np.int64(r["best_length"])
+        g[f"run{ri}_tour"] = r["best_tour"]
+        g[f"run{ri}_comparisons"] = np.uint64(r["comparisons"])
+        runs.append(ri)
+    g["run_cases"] = np.array(runs)
+
+    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    np.savez_compressed(OUT, **g)
+    print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
+
+
+if __name__ == "__main__":
+    main()

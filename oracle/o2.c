@@ -485,6 +485,36 @@ void o2_destroy(o2_state* s) {
     free(s);
 }
 
+/* evaporate then deposit every built tour in tour order (engine.hpp:253-259,
+   construction.hpp:187-207) -- restricted to candidate edges, which evolve
+   independently of every other matrix entry */
+static void classic_update(o2_state* s, const uint32_t* tours, const int64_t* lens, uint32_t ntours) {
+    const uint32_t n = s->n, k = s->k;
+    const double keep = 1.0 - s->p.rho;
+    for (size_t q = 0; q < (size_t)n * k; ++q) { double t = s->T[q] * keep; if (t < 1e-6) t = 1e-6; s->T[q] = t; }
+    uint32_t* pos = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    for (uint32_t a = 0; a < ntours; ++a) {
+        const uint32_t* t = tours + (size_t)a * n;
+        const double delta = 1.0 / (double)lens[a];
+        for (uint32_t p = 0; p < n; ++p) pos[t[p]] = p;
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t pi = pos[i];
+            const uint32_t pv = t[(pi + n - 1) % n], nx = t[(pi + 1) % n];
+            for (uint32_t r = 0; r < k; ++r) {
+                const uint32_t c = s->knn[(size_t)i * k + r];
+                if (c == pv || c == nx) s->T[(size_t)i * k + r] += delta;
+            }
+        }
+    }
+    free(pos);
+}
+
+int o2_classic_apply(o2_state* s, const uint32_t* tours, const int64_t* lens, uint32_t ntours) {
+    if (!s->T) FAIL("not a classic-mode state");
+    classic_update(s, tours, lens, ntours);
+    return 0;
+}
+
 int o2_iterate(o2_state* s, const uint32_t* words, uint64_t stride) {
     set_err_ok();
     if (s->p.draw_source == 1 && !words) FAIL("draw buffer required");
@@ -492,28 +522,7 @@ int o2_iterate(o2_state* s, const uint32_t* words, uint64_t stride) {
     compute_weights(s);
     if (par_for(s, 1, s->m, NULL, seeding, words, stride)) FAIL("draw buffer too short");
     const uint32_t n = s->n, m = s->m, k = s->k;
-    if (s->p.mode == 2) {
-        /* evaporate then deposit every built tour in tour order (engine.hpp:253-259,
-           construction.hpp:187-207) -- restricted to candidate edges, which evolve
-           independently of every other matrix entry */
-        const double keep = 1.0 - s->p.rho;
-        for (size_t q = 0; q < (size_t)n * k; ++q) { double t = s->T[q] * keep; if (t < 1e-6) t = 1e-6; s->T[q] = t; }
-        uint32_t* pos = (uint32_t*)malloc(sizeof(uint32_t) * n);
-        for (uint32_t a = 0; a < m; ++a) {
-            const uint32_t* t = s->tours + (size_t)a * n;
-            const double delta = 1.0 / (double)s->lens[a];
-            for (uint32_t p = 0; p < n; ++p) pos[t[p]] = p;
-            for (uint32_t i = 0; i < n; ++i) {
-                const uint32_t pi = pos[i];
-                const uint32_t pv = t[(pi + n - 1) % n], nx = t[(pi + 1) % n];
-                for (uint32_t r = 0; r < k; ++r) {
-                    const uint32_t c = s->knn[(size_t)i * k + r];
-                    if (c == pv || c == nx) s->T[(size_t)i * k + r] += delta;
-                }
-            }
-        }
-        free(pos);
-    }
+    if (s->p.mode == 2) classic_update(s, s->tours, s->lens, m);
     for (uint32_t a = 0; a < m; ++a) /* engine.hpp:261-265, ant order */
         s->improved[a] = (uint8_t)offer(s, a, s->tours + (size_t)a * n, s->lens[a]);
     s->iter++;

@@ -72,6 +72,8 @@ int o2_iterate(o2_state* s, const uint32_t* words, uint64_t stride);
 void o2_get_knn(const o2_state* s, uint32_t* out);
 void o2_tau_row(const o2_state* s, uint32_t i, double* out); /* tau^alpha over all j */
 void o2_get_T(const o2_state* s, double* out);               /* classic: n*k candidate-edge tau */
+/* classic: one evaporate + deposit of the given tours (construction.hpp:187-207) */
+int o2_classic_apply(o2_state* s, const uint32_t* tours, const int64_t* lens, uint32_t ntours);
 void o2_get_weights(const o2_state* s, float* out); /* n*k weights of the last iteration */
 void o2_get_tours(const o2_state* s, uint32_t* tours, int64_t* lens);
 void o2_get_lbest(const o2_state* s, uint32_t* tours, int64_t* lens);

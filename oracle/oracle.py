@@ -70,6 +70,7 @@ def o2lib():
                                       POINTER(c_uint32), POINTER(c_int64)]
         L.o2_tau_row.argtypes = [vp, c_uint32, POINTER(c_double)]
         L.o2_get_T.argtypes = [vp, POINTER(c_double)]
+        L.o2_classic_apply.argtypes = [vp, POINTER(c_uint32), POINTER(c_int64), c_uint32]
         L.o2_last_error.restype = ctypes.c_char_p
         L.o2_draw_word.restype = c_uint32
         L.o2_draw_word.argtypes = [c_uint64, c_uint32, c_uint64, c_uint32]
@@ -144,6 +145,12 @@ class O2:
         out = np.empty((self.n, self.k), np.float64)
         self.L.o2_get_T(self.h, _p(out, c_double))
         return out
+
+    def classic_apply(self, tours, lens):
+        t = np.ascontiguousarray(tours, np.uint32)
+        l = np.ascontiguousarray(lens, np.int64)
+        if self.L.o2_classic_apply(self.h, _p(t, c_uint32), _p(l, c_int64), l.size):
+            raise RuntimeError(self.L.o2_last_error().decode())
 
     def tours(self):
         t = np.empty((self.m, self.n), np.uint32)

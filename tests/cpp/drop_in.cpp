@@ -1,0 +1,56 @@
+// Drop-in check: the reference's calling convention (Instance, RunConfig, Mode -> RunReport)
+// against the B200 engine through include/paco_b200/paco.hpp. Exit code 0 = pass.
+// Usage: drop_in [expect-gpu 0|1]
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+
+#include "paco_b200/paco.hpp"
+
+#define CHECK(c) do { if (!(c)) { std::fprintf(stderr, "CHECK failed: %s (line %d)\n", #c, __LINE__); return 1; } } while (0)
+
+int main(int argc, char** argv) {
+    const bool gpu = argc > 1 && std::string(argv[1]) == "1";
+    // config validation mirrors RunConfig::validate (engine.hpp:61-75)
+    paco_b200::RunConfig bad;
+    bad.ants = 0;
+    bool threw = false;
+    try { bad.validate(); } catch (const std::invalid_argument& e) { threw = std::string(e.what()) == "ants must be >= 1"; }
+    CHECK(threw);
+    CHECK(paco_b200::mode_from_name("partial") == paco_b200::Mode::partial_aco);
+
+    // grid442 (26 x 17 lattice, spacing 10, optimum 4420)
+    std::vector<std::pair<double, double>> pts;
+    for (int r = 0; r < 17; ++r) for (int c = 0; c < 26; ++c) pts.emplace_back(10.0 * c, 10.0 * r);
+    paco_b200::Instance inst("grid442", pts, 4420);
+    paco_b200::RunConfig cfg;
+    cfg.ants = 16; cfg.iterations = 50; cfg.alpha = 1.0; cfg.beta = 2.0; cfg.candidates = 12; cfg.seed = 3;
+    try {
+        const auto rep = paco_b200::run(inst, cfg, paco_b200::Mode::partial_aco);
+        CHECK(gpu);
+        CHECK(rep.best_length >= 4420);
+        CHECK(rep.best_tour.order.size() == 442);
+        std::vector<int> seen(442, 0);
+        for (auto c : rep.best_tour.order) { CHECK(c < 442); CHECK(!seen[c]); seen[c] = 1; }
+        std::int64_t len = 0;
+        for (size_t i = 0; i < 442; ++i) len += inst.dist(rep.best_tour.order[i], rep.best_tour.order[(i + 1) % 442]);
+        CHECK(len == rep.best_length);
+        CHECK(rep.pct_error && *rep.pct_error >= 0.0);
+        CHECK(rep.iterations_done == 50);
+        std::printf("drop_in ok: best %lld (%.2f%% over optimum) decisions %llu wall %.3fs\n",
+                    (long long)rep.best_length, *rep.pct_error, (unsigned long long)rep.counters.decisions,
+                    rep.wall_time_s);
+        // classic mode refuses n > 5000 with the reference's message (engine.hpp:158-160)
+        std::vector<std::pair<double, double>> big;
+        for (int i = 0; i < 5001; ++i) big.emplace_back(i % 100, i / 100);
+        threw = false;
+        try { paco_b200::run(paco_b200::Instance("big", big), cfg, paco_b200::Mode::classic_aco); }
+        catch (const std::invalid_argument& e) { threw = std::string(e.what()).find("n <= 5000") != std::string::npos; }
+        CHECK(threw);
+    } catch (const std::runtime_error& e) {
+        if (gpu) { std::fprintf(stderr, "unexpected: %s\n", e.what()); return 1; }
+        std::printf("no GPU: %s\n", e.what());  // the engine has no CPU fallback
+    }
+    return 0;
+}

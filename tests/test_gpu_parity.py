@@ -228,3 +228,14 @@ def test_config_errors():
         Colony(inst, RunConfig(ants=0))
     with pytest.raises(PacoError):
         Colony(inst, RunConfig(ants=4, two_opt_prob=0.1))
+
+
+def test_cpp_drop_in_on_gpu(tmp_path):
+    import subprocess
+    from test_host import build_drop_in
+    from paper_1709_03187_b200 import _native
+    _native.load()
+    exe = build_drop_in(str(tmp_path))
+    out = subprocess.run([exe, "1"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert "drop_in ok" in out.stdout
