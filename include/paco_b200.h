@@ -43,6 +43,14 @@ typedef enum paco_mode { PACO_MODE_PARTIAL = 0, PACO_MODE_PACO = 1, PACO_MODE_CL
  * (validation mode, shared with the CPU oracle). */
 typedef enum paco_draws { PACO_DRAWS_PHILOX = 0, PACO_DRAWS_BUFFER = 1 } paco_draws;
 
+/* Selection rule. CANDIDATE_ROULETTE is the north-star rule (k-NN candidate list,
+ * roulette wheel, exact nearest-unvisited fallback; Philox or buffer draws).
+ * INDEPENDENT_ROULETTE is the reference's own rule (construction.hpp:243-281) with
+ * the reference's xoshiro256++ streams (rng.hpp:24-74): a run is bit-identical to
+ * paco::run in synchronous mode. It scans every unvisited city per decision and is
+ * provided for parity, not speed. */
+typedef enum paco_rule { PACO_RULE_CANDIDATE_ROULETTE = 0, PACO_RULE_INDEPENDENT_ROULETTE = 1 } paco_rule;
+
 /* RunConfig, engine.hpp:42-76, field for field, plus the north-star additions at the end. */
 typedef struct paco_config {
     uint32_t ants;                 /* m */
@@ -63,6 +71,7 @@ typedef struct paco_config {
     uint32_t candidates;           /* k of the k-NN candidate list, 1..32 (clamped to n-1) */
     uint32_t draws;                /* paco_draws */
     int32_t device;                /* CUDA device ordinal, -1 = current */
+    uint32_t rule;                 /* paco_rule */
 } paco_config;
 
 typedef struct paco_counters {
@@ -74,6 +83,7 @@ typedef struct paco_counters {
     uint64_t partial_builds;
     uint64_t iterations;
     uint64_t improvements;   /* successful update_l_best calls */
+    uint64_t comparisons;    /* candidate scores evaluated (IR rule: the reference's comparison count) */
 } paco_counters;
 
 /* RunReport, engine.hpp:84-92 (+ counters and device-time breakdown) */
@@ -82,7 +92,7 @@ typedef struct paco_report {
     double pct_error;          /* NaN when no optimum was supplied */
     double wall_time_s;
     uint64_t iterations_done;
-    uint64_t comparisons_total;/* IR-equivalent accounting is not produced by the k-NN rule: = decisions */
+    uint64_t comparisons_total;/* IR rule: the reference's count; candidate rule: decisions */
     paco_counters counters;
     double construct_ms;       /* device time in the construction kernel (CUDA events) */
     double update_ms;          /* weights + completion-step kernels */

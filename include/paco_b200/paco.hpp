@@ -72,6 +72,7 @@ struct RunConfig {
     bool validate_tours = false;
     std::uint32_t candidates = 16;  // k of the k-NN candidate list
     int device = -1;
+    paco_rule rule = PACO_RULE_CANDIDATE_ROULETTE;  // INDEPENDENT_ROULETTE = the reference's rule, bit-exact
 
     paco_config to_c() const {
         paco_config c{};
@@ -82,7 +83,7 @@ struct RunConfig {
         c.tau_max = tau_max; c.tau0 = tau0; c.time_budget_s = time_budget_s;
         c.convergence_interval_s = convergence_interval_s; c.synchronous = synchronous ? 1u : 0u;
         c.validate_tours = validate_tours ? 1u : 0u; c.candidates = candidates;
-        c.draws = PACO_DRAWS_PHILOX; c.device = device;
+        c.draws = PACO_DRAWS_PHILOX; c.device = device; c.rule = rule;
         return c;
     }
 

@@ -22,6 +22,7 @@ PACO_E_LOGIC = -5
 
 MODE_PARTIAL, MODE_PACO, MODE_CLASSIC = 0, 1, 2
 DRAWS_PHILOX, DRAWS_BUFFER = 0, 1
+RULE_CANDIDATE_ROULETTE, RULE_INDEPENDENT_ROULETTE = 0, 1
 
 # every symbol include/paco_b200.h declares
 EXPORTED = (
@@ -39,14 +40,14 @@ class Config(ctypes.Structure):
         ("two_opt_prob", c_double), ("two_opt_window", c_uint32), ("synchronous", c_uint32),
         ("seed", c_uint64), ("rho", c_double), ("tau_max", c_double), ("tau0", c_double),
         ("time_budget_s", c_double), ("convergence_interval_s", c_double), ("validate_tours", c_uint32),
-        ("candidates", c_uint32), ("draws", c_uint32), ("device", c_int32),
+        ("candidates", c_uint32), ("draws", c_uint32), ("device", c_int32), ("rule", c_uint32),
     ]
 
 
 class Counters(ctypes.Structure):
     _fields_ = [(name, c_uint64) for name in (
         "decisions", "fallbacks", "ties", "forced", "full_builds", "partial_builds", "iterations",
-        "improvements")]
+        "improvements", "comparisons")]
 
     def as_dict(self) -> dict:
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

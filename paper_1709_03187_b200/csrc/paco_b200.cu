@@ -18,6 +18,7 @@
 
 #include "../../include/paco_b200.h"
 #include "kernels.cuh"
+#include "kernels_ir.cuh"
 
 using namespace pacob200;
 
@@ -48,6 +49,7 @@ int kmax_for(uint32_t k) { return k <= 8 ? 8 : k <= 16 ? 16 : k <= 24 ? 24 : 32;
 
 struct paco_handle {
     int dev = 0;
+    int num_sms = 148;
     cudaStream_t st = nullptr;
     paco_config cfg{};
     int mode = 0;
@@ -79,12 +81,17 @@ struct paco_handle {
     double construct_ms = 0, update_ms = 0, setup_ms = 0;
     std::vector<cudaEvent_t> evpool;
     uint32_t knn_global_fallbacks = 0;
+    // reference-rule (IR) mode
+    bool ir = false;
+    uint64_t* rng = nullptr;   // m*4 xoshiro256++ states
+    double* ratio = nullptr;   // m
+    double* Tfull = nullptr;   // classic: n*n
 
     ~paco_handle() {
         if (dev >= 0) cudaSetDevice(dev);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
                         partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, counters, err, words,
-                        scratch_u32, scratch_u64};
+                        scratch_u32, scratch_u64, rng, ratio, Tfull};
         for (void* p : ptrs)
             if (p) cudaFree(p);
         for (auto e : evpool) cudaEventDestroy(e);
@@ -134,6 +141,9 @@ paco_status paco_config_validate(const paco_config* c, uint32_t n, int mode) {
     if (n < 3) return fail(PACO_E_INVALID, "instance needs at least 3 cities, got " + std::to_string(n));
     if (c->candidates < 1 || c->candidates > 32) return fail(PACO_E_INVALID, "candidates must be in [1,32]");
     if (c->draws > 1) return fail(PACO_E_INVALID, "unknown draw source");
+    if (c->rule > 1) return fail(PACO_E_INVALID, "unknown selection rule");
+    if (c->rule == PACO_RULE_INDEPENDENT_ROULETTE && c->draws != PACO_DRAWS_PHILOX)
+        return fail(PACO_E_INVALID, "the reference rule draws from its own xoshiro256++ streams");
     if (c->two_opt_prob > 0.0) return fail(PACO_E_UNSUPPORTED, "2-opt is not provided by the GPU engine yet");
     if (!c->synchronous) return fail(PACO_E_UNSUPPORTED, "asynchronous mode is not provided by the GPU engine yet");
     return PACO_OK;
@@ -167,32 +177,22 @@ static paco_status build_grid(paco_handle* h) {
     return PACO_OK;
 }
 
-static paco_status setup(paco_handle* h) {
-    const uint32_t n = h->n, m = h->m, k = h->k;
+// reference rule: [acc n doubles (P-ACO)] [32 draws] [bitmap]
+static size_t ir_smem_bytes(uint32_t n, uint32_t nwords, int mode) {
+    return (mode == PACO_MODE_CLASSIC ? 0 : (size_t)8 * n) + 32 * 8 + (size_t)nwords * 4;
+}
+
+// colony state shared by both selection rules
+static paco_status alloc_colony(paco_handle* h) {
+    const uint32_t n = h->n, m = h->m;
     cudaStream_t st = h->st;
-    if (build_grid(h) != PACO_OK) return PACO_E_RUNTIME;
-    double *dx = nullptr, *dy = nullptr;
-    unsigned long long *keys = nullptr, *keys2 = nullptr;
-    uint32_t* cellm = nullptr;
-    CU(dalloc(&dx, n)); CU(dalloc(&dy, n));
-    CU(dalloc(&keys, n)); CU(dalloc(&keys2, n)); CU(dalloc(&cellm, n));
     CU(dalloc(&h->xy, n)); CU(dalloc(&h->orig_of, n)); CU(dalloc(&h->int_of, n));
-    CU(dalloc(&h->cell_start, (size_t)h->g.ncells + 1));
-    CU(dalloc(&h->knn, (size_t)n * 32)); CU(dalloc(&h->eta, (size_t)n * k)); CU(dalloc(&h->cand, (size_t)n * h->kp));
-    CU(cudaMemsetAsync(h->cand, 0, sizeof(uint2) * (size_t)n * h->kp, st));
     CU(dalloc(&h->tours, (size_t)m * 2 * n));
     CU(dalloc(&h->lb_sel, m)); CU(dalloc(&h->has_lb, m)); CU(dalloc(&h->improved, m)); CU(dalloc(&h->partial, m));
     CU(dalloc(&h->new_len, m)); CU(dalloc(&h->lb_len, m)); CU(dalloc(&h->g_len, 1));
     CU(dalloc(&h->nbr, (size_t)m * n));
-    CU(dalloc(&h->gb, 1)); CU(dalloc(&h->counters, 8)); CU(dalloc(&h->err, 1));
+    CU(dalloc(&h->gb, 1)); CU(dalloc(&h->counters, 16)); CU(dalloc(&h->err, 1));
     CU(dalloc(&h->scratch_u32, (size_t)n + 64)); CU(dalloc(&h->scratch_u64, 4));
-    if (h->mode == PACO_MODE_CLASSIC) {
-        CU(dalloc(&h->T, (size_t)n * k));
-        CU(dalloc(&h->cur_nbr, (size_t)m * n));
-        std::vector<double> init((size_t)n * k, h->cfg.tau_max);
-        CU(cudaMemcpyAsync(h->T, init.data(), sizeof(double) * init.size(), cudaMemcpyHostToDevice, st));
-        CU(cudaStreamSynchronize(st));
-    }
     CU(cudaMemsetAsync(h->lb_sel, 0, m, st)); CU(cudaMemsetAsync(h->has_lb, 0, m, st));
     CU(cudaMemsetAsync(h->improved, 0, m, st)); CU(cudaMemsetAsync(h->partial, 0, m, st));
     CU(cudaMemsetAsync(h->lb_len, 0, sizeof(int64_t) * m, st));
@@ -202,8 +202,79 @@ static paco_status setup(paco_handle* h) {
     const int64_t gmax = std::numeric_limits<int64_t>::max();
     CU(cudaMemcpyAsync(h->gb, &g0, sizeof g0, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(h->g_len, &gmax, sizeof gmax, cudaMemcpyHostToDevice, st));
-    CU(cudaMemsetAsync(h->counters, 0, 8 * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(h->counters, 0, 16 * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(h->err, 0, sizeof(int), st));
+    if (h->mode == PACO_MODE_CLASSIC) CU(dalloc(&h->cur_nbr, (size_t)m * n));
+    CU(cudaStreamSynchronize(st));
+    return PACO_OK;
+}
+
+// SplitMix64 + Rng::for_stream (rng.hpp:10-38), restated to seed the reference-rule
+// streams exactly as Colony does for ant k (colony.hpp:93-95).
+static uint64_t splitmix_next(uint64_t& s) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+static void rng_for_stream(uint64_t master, uint64_t stream, uint64_t out[4]) {
+    uint64_t sm = master;
+    const uint64_t a = splitmix_next(sm);
+    uint64_t mix = a ^ (stream * 0x9e3779b97f4a7c15ULL + 0x2545f4914f6cdd1dULL);
+    uint64_t seed = splitmix_next(mix);
+    for (int q = 0; q < 4; ++q) out[q] = splitmix_next(seed);
+}
+
+// Reference-rule mode: cities stay in their original order (the rule consumes draws
+// in ascending city index), no candidate lists.
+static paco_status setup_ir(paco_handle* h) {
+    const uint32_t n = h->n, m = h->m;
+    paco_status s = alloc_colony(h);
+    if (s != PACO_OK) return s;
+    std::vector<double2> xy(n);
+    std::vector<uint32_t> ident(n);
+    for (uint32_t i = 0; i < n; ++i) { xy[i] = make_double2(h->hx[i], h->hy[i]); ident[i] = i; }
+    CU(cudaMemcpy(h->xy, xy.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->orig_of, ident.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->int_of, ident.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+    h->h_orig = ident;
+    h->h_int = ident;
+    std::vector<uint64_t> st((size_t)m * 4);
+    for (uint32_t a = 0; a < m; ++a) rng_for_stream(h->cfg.seed, a, &st[(size_t)a * 4]);
+    CU(dalloc(&h->rng, (size_t)m * 4));
+    CU(cudaMemcpy(h->rng, st.data(), sizeof(uint64_t) * st.size(), cudaMemcpyHostToDevice));
+    CU(dalloc(&h->ratio, m));
+    CU(cudaMemset(h->ratio, 0, sizeof(double) * m));
+    if (h->mode == PACO_MODE_CLASSIC) {  // PheromoneMatrix(n, rho, tau_max), construction.hpp:165-175
+        CU(dalloc(&h->Tfull, (size_t)n * n));
+        std::vector<double> init((size_t)n * n, h->cfg.tau_max);
+        CU(cudaMemcpy(h->Tfull, init.data(), sizeof(double) * init.size(), cudaMemcpyHostToDevice));
+    }
+    h->setup_ms = 0.0;
+    return PACO_OK;
+}
+
+static paco_status setup(paco_handle* h) {
+    if (h->ir) return setup_ir(h);
+    const uint32_t n = h->n, k = h->k;
+    cudaStream_t st = h->st;
+    if (build_grid(h) != PACO_OK) return PACO_E_RUNTIME;
+    paco_status s0 = alloc_colony(h);
+    if (s0 != PACO_OK) return s0;
+    double *dx = nullptr, *dy = nullptr;
+    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    uint32_t* cellm = nullptr;
+    CU(dalloc(&dx, n)); CU(dalloc(&dy, n));
+    CU(dalloc(&keys, n)); CU(dalloc(&keys2, n)); CU(dalloc(&cellm, n));
+    CU(dalloc(&h->cell_start, (size_t)h->g.ncells + 1));
+    CU(dalloc(&h->knn, (size_t)n * 32)); CU(dalloc(&h->eta, (size_t)n * k)); CU(dalloc(&h->cand, (size_t)n * h->kp));
+    CU(cudaMemsetAsync(h->cand, 0, sizeof(uint2) * (size_t)n * h->kp, st));
+    if (h->mode == PACO_MODE_CLASSIC) {
+        CU(dalloc(&h->T, (size_t)n * k));
+        std::vector<double> init((size_t)n * k, h->cfg.tau_max);
+        CU(cudaMemcpyAsync(h->T, init.data(), sizeof(double) * init.size(), cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    }
 
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
@@ -267,11 +338,17 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
     if (prop.major != 10) return fail(PACO_E_CUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
     const uint32_t nwords = (n + 31) / 32;
     const uint32_t kk = std::min<uint32_t>(cfg->candidates, n - 1), kpp = (kk + 1) & ~1u;
-    if ((size_t)nwords * 4 + (size_t)2 * kk * kpp * 8 > (size_t)prop.sharedMemPerBlockOptin)
-        return fail(PACO_E_UNSUPPORTED, "visited bitmap exceeds shared memory (n too large)");
+    (void)kpp;
+    const bool ir = cfg->rule == PACO_RULE_INDEPENDENT_ROULETTE;
+    const size_t smem_need = ir ? ir_smem_bytes(n, nwords, mode) : 512 + (size_t)nwords * 4;
+    if (smem_need > (size_t)prop.sharedMemPerBlockOptin)
+        return fail(PACO_E_UNSUPPORTED, ir ? "reference-rule per-ant state exceeds shared memory (n too large)"
+                                           : "visited bitmap exceeds shared memory (n too large)");
     auto* h = new (std::nothrow) paco_handle();
     if (!h) return fail(PACO_E_RUNTIME, "out of host memory");
+    h->ir = ir;
     h->dev = dev;
+    h->num_sms = prop.multiProcessorCount;
     h->cfg = *cfg;
     h->mode = mode;
     h->n = n; h->m = cfg->ants; h->k = std::min<uint32_t>(cfg->candidates, n - 1); h->nwords = nwords;
@@ -317,6 +394,34 @@ static paco_status launch_weights(paco_handle* h) {
     return PACO_OK;
 }
 
+static paco_status launch_ratios(paco_handle* h) {
+    if (h->mode == PACO_MODE_CLASSIC) return PACO_OK;
+    k_ratios<<<(h->m + 127) / 128, 128, 0, h->st>>>(h->lb_len, h->has_lb, h->g_len, h->m, h->ratio);
+    CU(cudaGetLastError());
+    return PACO_OK;
+}
+
+static paco_status launch_construct_ir(paco_handle* h, bool seeding) {
+    IrArgs a{};
+    a.xy = h->xy; a.nbr = h->nbr; a.ratio = h->ratio;
+    a.T = h->mode == PACO_MODE_CLASSIC ? h->Tfull : nullptr;
+    a.rng = h->rng; a.tours = h->tours; a.lb_sel = h->lb_sel; a.new_len = h->new_len;
+    a.partial_flag = h->partial; a.counters = h->counters;
+    a.n = h->n; a.m = h->m; a.nwords = h->nwords;
+    a.alpha = h->cfg.alpha; a.beta = h->cfg.beta; a.tau0 = h->cfg.tau0;
+    a.eff_pp = h->mode == PACO_MODE_PARTIAL ? h->cfg.partial_prob : 0.0;  // engine.hpp:164-165
+    a.mmf = h->cfg.max_mod_frac;
+    a.seeding = seeding ? 1 : 0;
+    a.coin_always = 0;
+    a.eta_table = h->n <= 5000 ? 1 : 0;  // Heuristic keeps an f32 table iff the instance has a matrix
+    const size_t smem = ir_smem_bytes(h->n, h->nwords, h->mode);
+    if (smem > 48 * 1024)
+        CU(cudaFuncSetAttribute(k_construct_ir, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_construct_ir<<<h->m, 32, smem, h->st>>>(a);
+    CU(cudaGetLastError());
+    return PACO_OK;
+}
+
 static ConstructArgs construct_args(paco_handle* h, bool seeding) {
     ConstructArgs a{};
     a.cand = h->cand; a.knn32 = h->knn; a.xy = h->xy; a.orig_of = h->orig_of; a.int_of = h->int_of;
@@ -341,9 +446,15 @@ static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint
     const size_t smem = 512 + (size_t)h->nwords * 4;
 #endif
     const bool buf = a.words != nullptr;
+    // Shared-memory carveout: just enough for the CTAs one SM must host to run every ant at
+    // once (ceil(m / #SMs) warps), so the rest of the unified L1 caches candidate rows.
+    const int per_sm = (int)((blocks + h->num_sms - 1) / h->num_sms);
+    const int carve = (int)std::min<size_t>(100, (size_t)per_sm * (smem + 1024) * 100 / (228 * 1024) + 1);
     auto launch = [&](auto kern) -> paco_status {
         if (smem > 48 * 1024)
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (getenv("PACO_CARVEOUT")) CU(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(getenv("PACO_CARVEOUT"))));
+        else CU(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         kern<<<blocks, 32, smem, h->st>>>(a);
         CU(cudaGetLastError());
         return PACO_OK;
@@ -376,13 +487,19 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
         const bool seeding = h->mode != PACO_MODE_CLASSIC && h->iter == 0;
         const size_t e0 = e++, e1 = e++, e2 = e++;
         CU(cudaEventRecord(ev(h, e0), h->st));
-        paco_status s = launch_weights(h);
+        paco_status s = h->ir ? launch_ratios(h) : launch_weights(h);
         if (s != PACO_OK) return s;
         CU(cudaEventRecord(ev(h, e1), h->st));
-        s = launch_construct(h, construct_args(h, seeding), m);
+        s = h->ir ? launch_construct_ir(h, seeding) : launch_construct(h, construct_args(h, seeding), m);
         if (s != PACO_OK) return s;
         CU(cudaEventRecord(ev(h, e2), h->st));
-        if (h->mode == PACO_MODE_CLASSIC) {
+        if (h->ir && h->mode == PACO_MODE_CLASSIC) {
+            // full-matrix evaporate + deposit (construction.hpp:187-207), engine.hpp:253-259
+            dim3 grid((n + 255) / 256, m);
+            k_publish<<<grid, 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, n, 1, h->cur_nbr);
+            k_classic_full<<<(n + 127) / 128, 128, 0, h->st>>>(h->cur_nbr, h->new_len, n, m, h->cfg.rho, h->Tfull);
+            CU(cudaGetLastError());
+        } else if (h->mode == PACO_MODE_CLASSIC) {
             // evaporate + deposit on the built tours before the l_best updates (engine.hpp:253-259)
             dim3 grid((n + 255) / 256, m);
             k_publish<<<grid, 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, n, 1, h->cur_nbr);
@@ -498,10 +615,11 @@ paco_status paco_get_g_best(paco_handle* h, uint32_t* tour, int64_t* length) {
 paco_status paco_get_counters(paco_handle* h, paco_counters* c) {
     if (!h || !c) return fail(PACO_E_INVALID, "null argument");
     CU(cudaSetDevice(h->dev));
-    unsigned long long v[8];
+    unsigned long long v[16];
     CU(cudaMemcpy(v, h->counters, sizeof v, cudaMemcpyDeviceToHost));
     c->decisions = v[0]; c->fallbacks = v[1]; c->ties = v[2]; c->forced = v[3];
     c->full_builds = v[4]; c->partial_builds = v[5]; c->iterations = h->iter; c->improvements = v[7];
+    c->comparisons = h->ir ? v[8] : v[0];
     return PACO_OK;
 }
 
@@ -515,6 +633,7 @@ paco_status paco_get_build_flags(paco_handle* h, uint8_t* partial, uint8_t* impr
 
 paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, uint32_t* k_out) {
     if (!h) return fail(PACO_E_INVALID, "null handle");
+    if (h->ir) return fail(PACO_E_UNSUPPORTED, "the reference rule has no candidate lists");
     CU(cudaSetDevice(h->dev));
     const uint32_t n = h->n, k = h->k;
     if (k_out) *k_out = k;
@@ -596,6 +715,7 @@ paco_status paco_construct_at(paco_handle* h, uint32_t ant, uint32_t start_pos, 
     if (m_mod > n) return fail(PACO_E_INVALID, "m_mod exceeds city count");  // construction.hpp:318
     if (start_pos >= n) return fail(PACO_E_INVALID, "start_pos out of range");
     if (nwords < 4ull + n) return fail(PACO_E_INVALID, "need n + 4 draw words");
+    if (h->ir) return fail(PACO_E_UNSUPPORTED, "construct_at is defined for the candidate-list rule");
     CU(cudaSetDevice(h->dev));
     uint8_t has = 0;
     CU(cudaMemcpy(&has, h->has_lb + ant, 1, cudaMemcpyDeviceToHost));
@@ -666,7 +786,7 @@ paco_status paco_run(const double* xs, const double* ys, uint32_t n, const paco_
     rep->pct_error = optimum > 0 ? 100.0 * ((double)len - (double)optimum) / (double)optimum
                                  : std::numeric_limits<double>::quiet_NaN();
     rep->iterations_done = done;
-    rep->comparisons_total = rep->counters.decisions;
+    rep->comparisons_total = rep->counters.comparisons;
     rep->construct_ms = c_ms; rep->update_ms = u_ms;
     if (best_tour) std::memcpy(best_tour, tour.data(), sizeof(uint32_t) * n);
     rep->wall_time_s = since();

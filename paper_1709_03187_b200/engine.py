@@ -58,12 +58,17 @@ class RunConfig:
     candidates: int = 16
     draws: str = "philox"  # or "buffer" (validation mode)
     device: int = -1
+    rule: str = "roulette"  # north-star candidate-list roulette; "independent" = the reference's IR rule
 
     def to_c(self) -> N.Config:
         c = N.Config()
         for name, _ in N.Config._fields_:
             if name == "draws":
                 c.draws = N.DRAWS_BUFFER if self.draws == "buffer" else N.DRAWS_PHILOX
+            elif name == "rule":
+                if self.rule not in ("roulette", "independent"):
+                    raise ValueError(f"unknown rule {self.rule!r}")
+                c.rule = N.RULE_INDEPENDENT_ROULETTE if self.rule == "independent" else N.RULE_CANDIDATE_ROULETTE
             else:
                 setattr(c, name, getattr(self, name))
         return c
