@@ -269,30 +269,34 @@ struct ConstructArgs {
     uint32_t force_ant, force_start_pos, force_m_mod;
 };
 
+// squared lower bound of the distance from q to the square [rx0, rx0+side) x [ry0, ry0+side),
+// with the square grown by `slack` on every side (no sqrt: compared against squared bests)
 __device__ __forceinline__ double rect_lb2(double2 q, double rx0, double ry0, double side, double slack) {
-    const double dx = fmax(0.0, fmax(rx0 - q.x, q.x - (rx0 + side)));
-    const double dy = fmax(0.0, fmax(ry0 - q.y, q.y - (ry0 + side)));
-    const double lb = sqrt(dx * dx + dy * dy) - slack;
-    return lb > 0 ? lb * lb : 0.0;
+    const double dx = fmax(0.0, fmax(rx0 - slack - q.x, q.x - (rx0 + side + slack)));
+    const double dy = fmax(0.0, fmax(ry0 - slack - q.y, q.y - (ry0 + side + slack)));
+    return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
 }
 
 struct FbStats {
 #ifdef PACO_TIMING
-    long long searches = 0, rings = 0, sbs = 0, cities = 0;
+    long long searches = 0, rings = 0, sbs = 0, cities = 0, t_test = 0, t_scan = 0, t_argmin = 0, t_pre = 0;
 #endif
 };
+
+constexpr uint32_t kFbList = 256;  // per-warp shared-memory list of unvisited city ids (fallback)
 
 // Exact nearest unvisited city by (d^2, original index), warp-cooperative.
 // F0: the 32-nearest list is sorted by the same key, so its first unvisited entry
 //     is the answer whenever one exists (one 128-byte row, one ballot).
 // F1: rings of 8x8-cell superblocks (each a contiguous id range) around cur with
-//     rectangle lower bounds. A superblock with no unvisited city is skipped with
-//     the shared-memory bitmap; the others are scanned flat, 128 ids per pass
-//     (four bitmap words broadcast to the warp, one predicated coordinate load per
-//     unvisited lane), so one pass costs a single L2 round trip. One warp argmin
-//     per ring; the ring loop stops when the next ring's bound exceeds the best.
+//     squared rectangle lower bounds. Per ring pass, each lane takes one superblock,
+//     counts its unvisited cities from the shared-memory bitmap, a warp scan turns the
+//     counts into offsets, the ids are appended to a shared list and the whole list is
+//     scored with one coordinate load per lane — one L2 round trip per ring instead of
+//     one per superblock. Original indices (the tie-break key) are loaded only on an
+//     exact distance tie and once per lane before the per-ring warp argmin.
 __device__ __forceinline__ uint32_t nearest_unvisited(const ConstructArgs& a, const uint32_t* vis, uint32_t cur,
-                                                   uint32_t lane, FbStats& fs) {
+                                                   uint32_t lane, uint32_t* list, FbStats& fs) {
     {
         const uint32_t c = ldg_u32(&a.knn32[(size_t)cur * 32 + lane]);
         const unsigned b = __ballot_sync(kFull, c != kNone && !is_visited(vis, c));
@@ -300,16 +304,27 @@ __device__ __forceinline__ uint32_t nearest_unvisited(const ConstructArgs& a, co
     }
 #ifdef PACO_TIMING
     ++fs.searches;
+    long long tp0 = clock64();
 #endif
     const GridParams& g = a.g;
     const double2 q = a.xy[cur];
     const int32_t cx = cell_coord(q.x, g.x0, g.inv, g.gw), cy = cell_coord(q.y, g.y0, g.inv, g.gh);
     double bd = __longlong_as_double(0x7ff0000000000000LL);
-    uint32_t bo = kNone, bj = kNone;
+    uint32_t bo = kNone, bj = kNone;  // bo == kNone with bj != kNone: original index not loaded yet
     const double slack = 1e-6 * g.cs;
     const int32_t sx = cx >> 3, sy = cy >> 3;
     const int32_t rmax = g.gws > g.ghs ? g.gws : g.ghs;
     const double span = 8.0 * g.cs;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    auto score = [&](uint32_t j) {
+        const double d = dist2(q, a.xy[j]);
+        if (d < bd) { bd = d; bj = j; bo = kNone; }
+        else if (d == bd) {
+            if (bo == kNone && bj != kNone) bo = a.orig_of[bj];
+            const uint32_t o = a.orig_of[j];
+            if (o < bo) { bj = j; bo = o; }
+        }
+    };
     for (int32_t rho = 0; rho <= rmax; ++rho) {
         if (rho >= 1) {
             const double lb = (rho - 1) * span - slack;
@@ -317,14 +332,18 @@ __device__ __forceinline__ uint32_t nearest_unvisited(const ConstructArgs& a, co
         }
 #ifdef PACO_TIMING
         ++fs.rings;
+        if (rho == 0) fs.t_pre += clock64() - tp0;
 #endif
         const double bound = bd;  // warp-uniform (argmin at the end of every ring)
-        const int32_t cnt = rho == 0 ? 1 : 8 * rho;
-        for (int32_t base = 0; base < cnt; base += 32) {
+        const int32_t cnt_ring = rho == 0 ? 1 : 8 * rho;
+        for (int32_t base = 0; base < cnt_ring; base += 32) {
+#ifdef PACO_TIMING
+            long long tt0 = clock64();
+#endif
             const int32_t c = base + (int32_t)lane;
             bool cand = false;
             uint32_t rs = 0, re = 0;
-            if (c < cnt) {
+            if (c < cnt_ring) {
                 int32_t x = sx, y = sy;
                 if (rho) ring_cell(rho, c, sx, sy, x, y);
                 if (x >= 0 && y >= 0 && x < g.gws && y < g.ghs &&
@@ -336,6 +355,9 @@ __device__ __forceinline__ uint32_t nearest_unvisited(const ConstructArgs& a, co
                 }
             }
             unsigned ball = __ballot_sync(kFull, cand);
+#ifdef PACO_TIMING
+            long long tt1; asm volatile("mov.u64 %0, %%clock64;" : "=l"(tt1) : "r"(ball)); fs.t_test += tt1 - tt0;
+#endif
             while (ball) {
                 const int src = __ffs(ball) - 1;
                 ball &= ball - 1;
@@ -343,30 +365,44 @@ __device__ __forceinline__ uint32_t nearest_unvisited(const ConstructArgs& a, co
 #ifdef PACO_TIMING
                 ++fs.sbs;
 #endif
+                // compact the superblock's unvisited ids into the shared list, 128 ids per
+                // pass: lane l tests bit l of four broadcast bitmap words
+                uint32_t n_list = 0;
                 for (uint32_t j0 = s & ~31u; j0 < e; j0 += 128) {
-                    uint32_t jj[4];
-                    bool un[4];
+                    uint32_t fb[4];
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
-                        jj[q4] = j0 + 32 * q4 + lane;
-                        const uint32_t wd = (j0 + 32 * q4 < e) ? vis[(j0 >> 5) + q4] : 0xffffffffu;
-                        un[q4] = jj[q4] >= s && jj[q4] < e && !((wd >> lane) & 1u);
+                        const uint32_t w = (j0 >> 5) + q4;
+                        fb[q4] = (j0 + 32 * q4 < e) ? free_bits(vis, w, s, e) : 0u;
                     }
-                    double d[4];
-                    uint32_t o[4];
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4)
-                        if (un[q4]) { d[q4] = dist2(q, a.xy[jj[q4]]); o[q4] = a.orig_of[jj[q4]]; }
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4)
-                        if (un[q4] && key_less(d[q4], o[q4], bd, bo)) { bd = d[q4]; bo = o[q4]; bj = jj[q4]; }
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        if ((fb[q4] >> lane) & 1u) list[n_list + __popc(fb[q4] & lt_mask)] = j0 + 32 * q4 + lane;
+                        n_list += __popc(fb[q4]);
+                    }
+                    if (n_list > kFbList - 128 || j0 + 128 >= e) {
+                        __syncwarp();
+                        for (uint32_t t = lane; t < n_list; t += 32) score(list[t]);
 #ifdef PACO_TIMING
-                    fs.cities += un[0] + un[1] + un[2] + un[3];
+                        if (lane == 0) fs.cities += n_list;
 #endif
+                        n_list = 0;
+                        __syncwarp();
+                    }
                 }
             }
+#ifdef PACO_TIMING
+            { long long tt2; asm volatile("mov.u64 %0, %%clock64;" : "=l"(tt2) : "l"(__double_as_longlong(bd))); fs.t_scan += tt2 - tt1; }
+#endif
         }
+#ifdef PACO_TIMING
+        long long ta0 = clock64();
+#endif
+        if (bo == kNone && bj != kNone) bo = a.orig_of[bj];
         warp_argmin(bd, bo, bj);
+#ifdef PACO_TIMING
+        { long long ta1; asm volatile("mov.u64 %0, %%clock64;" : "=l"(ta1) : "r"(bj)); fs.t_argmin += ta1 - ta0; }
+#endif
     }
     return bj;
 }
@@ -419,33 +455,27 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // One warp per ant (construction.hpp:283-365 with the north-star selection rule,
 // engine.hpp:129-148 draw order). The visited bitmap (n bits) lives in shared
 // memory. The dependent chain of one decision is:
-//   candidate row of the current city (8 B per lane, coalesced) -> bitmap probe
-//   -> warp inclusive scan -> ballot -> shuffle of the winner.
-// The row does not come from L2 on that chain: while a decision is being made,
-// every lane with a feasible candidate copies that candidate's row into a
-// per-warp shared-memory stage with LDGSTS (cp.async), so the next decision finds
-// its row on chip whichever candidate wins. Off-chain work (visited bit of the
-// city just entered, draw word, tour store, tie log) is scheduled around the
-// chain; Philox draws come 128 at a time, one 4-word block per lane, handed out
-// by shuffle. Preserved-segment copy, tour length and the optional permutation
-// check are warp-parallel passes fused before/after the chain.
+//   candidate row of the current city (8 B per lane, one coalesced line at k = 16)
+//   -> bitmap probe -> warp inclusive scan -> ballot -> shuffle of the winner.
+// Everything else is scheduled around that chain: the next row is requested the
+// moment the winner is known, before any bookkeeping; the visited bit of the new city
+// is one lane's fire-and-forget shared-memory OR, ordered for the other lanes by the
+// __syncwarp that opens the next decision; Philox draws come 128 at a time (one 4-word
+// block per lane) and the next decision's draw is fetched while its row is in flight;
+// all lane-divergent bookkeeping is predicated PTX. Preserved-segment copy, tour length
+// and the optional permutation check are warp-parallel passes around the chain.
 //
-// KP = row stride (k rounded up to even; 0 = generic runtime value), STEPS = scan
-// steps, BUF = draws from the validation buffer instead of Philox.
+// KP = row stride (k rounded up to even; 0 = runtime value), STEPS = scan steps
+// (ceil(log2 k); extra steps never touch lanes < k), BUF = validation-buffer draws.
 template <int KP, int STEPS, bool BUF>
 __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];  // [2][k][kp] row stage | bitmap
+    extern __shared__ __align__(16) unsigned char smem_raw[];  // fallback list | visited bitmap | warm scratch
     const uint32_t lane = threadIdx.x;
     const uint32_t ant = a.force ? a.force_ant : blockIdx.x;
     const uint32_t n = a.n, k = a.k, nw = a.nwords;
     const uint32_t kp = KP ? (uint32_t)KP : a.kp;
-    const uint32_t slot_bytes = kp * 8, buf_bytes = k * slot_bytes;
-#ifdef PACO_STAGE
-    const uint32_t stage_bytes = 2 * buf_bytes;
-#else
-    const uint32_t stage_bytes = 512;  // L1-warming scratch: 16 B per lane
-#endif
-    uint32_t* vis = reinterpret_cast<uint32_t*>(smem_raw + stage_bytes);
+    uint32_t* fb_list = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* vis = reinterpret_cast<uint32_t*>(smem_raw + kFbList * 4);
     const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
     const uint32_t* wrow = BUF ? a.words + (a.force ? 0 : (uint64_t)ant * a.stride) : nullptr;
     auto word = [&](uint32_t slot) -> uint32_t {
@@ -501,92 +531,55 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     uint32_t n_dec = 0, n_fb = 0, n_tie = 0, n_forced = 0;
     uint4 pb = make_uint4(0, 0, 0, 0);  // Philox block of this lane for the current 128-decision batch
     uint32_t remaining = n - pos;
-    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t vis_s = stage_s + stage_bytes;
-    const uint32_t warm_s = stage_s;
+    const uint32_t vis_s = (uint32_t)__cvta_generic_to_shared(vis);
+    const uint32_t warm_s = ((vis_s + nw * 4 + 15) & ~15u) + lane * 16;  // L1-warming scratch
     // lanes >= k never load: they hold (cur, 0.0f), and cur is always marked visited
     const bool lane_in = lane < k;
     const uint2* __restrict__ row_base = a.cand + lane;
     const uint32_t iter_lo = (uint32_t)a.iter, iter_hi = (uint32_t)(a.iter >> 32);
     FbStats fs;
-    uint32_t stage_row = 0xffffffffu;  // shared address of cur's staged row (this lane's entry), or none
-    uint32_t sbuf = 0;
 #ifdef PACO_TIMING
     const long long loop0 = clock64();
-    long long seg0 = 0, seg1 = 0, seg2 = 0, segn = 0, fbc = 0, segw = 0, sege = 0;
+    long long seg0 = 0, seg1 = 0, seg2 = 0, segn = 0, fbc = 0;
 #endif
     uint32_t uw = 0;  // draw word of the current decision (slot 4 + t)
-    // candidate row entry of the current decision
-    uint2 e_pre = ldg_u64_if(row_base + (size_t)cur * kp, lane_in && remaining > 1, make_uint2(cur, 0u));
     if (!BUF) {
         pb = philox10(make_uint4(1 + lane, ant, iter_lo, iter_hi), key);
         uw = __shfl_sync(kFull, pb.x, 0);
     } else if (remaining > 1) {
         uw = wrow[4];
     }
+    // candidate row entry of the current decision
+    uint2 e_pre = ldg_u64_if(row_base + (size_t)cur * kp, lane_in && remaining > 1, make_uint2(cur, 0u));
     for (uint32_t t = 0; remaining > 0; ++t, --remaining) {
         uint32_t next;
         ++n_dec;
         if (remaining > 1) {
+            __syncwarp();  // orders the previous decision's visited-bit update for every lane
             PACO_CLOCK(ta, t);
-            // 1. head of the dependent chain: cur's candidate row, on chip when the previous
-            //    decision staged it, else from L2
-#ifdef PACO_STAGE
-            uint2 e = make_uint2(cur, 0u);
-            cp_async_wait_all();
-            __syncwarp();
-            PACO_CLOCK(tw, t);
-            if (stage_row != 0xffffffffu) { if (lane_in) e = lds_u64(stage_row); }
-            else if (lane_in) e = ldg_u64(row_base + (size_t)cur * kp);
-#else
-            __syncwarp();
-            PACO_CLOCK(tw, t);
-            const uint2 e = e_pre;  // issued at the end of the previous decision
-#endif
-            PACO_CLOCK(te, e.x);
-            // 2. feasibility from the bitmap
+            const uint2 e = e_pre;  // requested at the end of the previous decision
+            // feasibility from the bitmap
             const uint32_t vw = lds_u32(vis_s + ((e.x >> 5) << 2));
             const float w = ((vw >> (e.x & 31)) & 1u) ? 0.0f : __uint_as_float(e.y);
             PACO_CLOCK(tb, __float_as_uint(w));
-            // 3. Hillis-Steele inclusive scan over the candidate lanes; the staging copies of
-            //    the feasible candidates' rows issue in the shadow of the first shuffle
+            // Hillis-Steele inclusive scan over the candidate lanes
             float v = w;
+            // Pull every feasible candidate's row into L1 with predicated cp.async.ca (one
+            // 16-byte copy per 32-byte sector into a per-lane scratch slot that is never
+            // read): the winner's row is then an L1 hit for the next decision.
+            // prefetch.global.L1 has no measurable effect on B200 (profiles/README.md).
             {
-                const float y = __shfl_up_sync(kFull, v, 1u);
-#ifndef PACO_STAGE
-                // warm L1 with every feasible candidate's row: an LDGSTS (cp.async.ca) per 32-byte
-                // sector into a per-lane scratch slot that is never read. On B200 this is what
-                // makes the next decision's row load an L1 hit: prefetch.global.L1 measured no
-                // effect (scratch microbenchmark, profiles/README.md).
-                {
-                    const bool cp = w > 0.0f;
-                    const unsigned char* src = reinterpret_cast<const unsigned char*>(a.cand + (size_t)e.x * kp);
-                    const uint32_t dst = warm_s + lane * 16;
-                    if (KP) {
-#pragma unroll
-                        for (int c = 0; c < (KP * 8 + 31) / 32; ++c) cp_async16_if(dst, src + 32 * c, cp);
-                    } else {
-                        for (uint32_t c = 0; c < (kp * 8 + 31) / 32; ++c) cp_async16_if(dst, src + 32 * c, cp);
-                    }
-                }
-#endif
-#ifdef PACO_STAGE
-                sbuf ^= 1u;
                 const bool cp = w > 0.0f;
                 const unsigned char* src = reinterpret_cast<const unsigned char*>(a.cand + (size_t)e.x * kp);
-                const uint32_t dst = stage_s + sbuf * buf_bytes + lane * slot_bytes;
                 if (KP) {
 #pragma unroll
-                    for (int c = 0; c < KP / 2; ++c) cp_async16_if(dst + 16 * c, src + 16 * c, cp);
+                    for (int c = 0; c < (KP * 8 + 31) / 32; ++c) cp_async16_if(warm_s, src + 32 * c, cp);
                 } else {
-                    for (uint32_t c = 0; c < kp / 2; ++c) cp_async16_if(dst + 16 * c, src + 16 * c, cp);
+                    for (uint32_t c = 0; c < (kp * 8 + 31) / 32; ++c) cp_async16_if(warm_s, src + 32 * c, cp);
                 }
-                cp_async_commit();
-#endif
-                if (lane >= 1u) v = __fadd_rn(v, y);
             }
 #pragma unroll
-            for (int st = 1; st < STEPS; ++st) {
+            for (int st = 0; st < STEPS; ++st) {
                 const float y = __shfl_up_sync(kFull, v, 1u << st);
                 if (lane >= (1u << st)) v = __fadd_rn(v, y);
             }
@@ -604,21 +597,19 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
                 const unsigned tie = __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(v, target)) <= tol);
                 const int r = ball ? __ffs(ball) - 1 : 31 - __clz(feas);
                 next = __shfl_sync(kFull, e.x, r);
-                stage_row = stage_s + sbuf * buf_bytes + (uint32_t)r * slot_bytes + lane * 8;
                 n_tie += tie ? 1u : 0u;
                 PACO_CLOCK(td, next);
 #ifdef PACO_TIMING
-                seg0 += tb - ta; seg1 += tc - tb; seg2 += td - tc; ++segn; segw += tw - ta; sege += te - tw; if (lane == 0 && stage_row == 0xffffffffu) {}
+                seg0 += tb - ta; seg1 += tc - tb; seg2 += td - tc; ++segn;
 #endif
             } else {
 #ifdef PACO_TIMING
                 const long long c0 = clock64();
 #endif
-                next = nearest_unvisited(a, vis, cur, lane, fs);
+                next = nearest_unvisited(a, vis, cur, lane, fb_list, fs);
 #ifdef PACO_TIMING
                 fbc += clock64() - c0;
 #endif
-                stage_row = 0xffffffffu;
                 ++n_fb;
             }
         } else {
@@ -626,14 +617,11 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
             next = last_unvisited(vis, nw, lane);
             ++n_forced;
         }
-        // off-chain bookkeeping after the pick, overlapping the loop turn: the visit of next
-        // (one lane, fire-and-forget; the __syncwarp at the top of the next decision orders
-        // it for every lane, and no candidate of next is next itself), the tour entry and
-        // the next decision's draw word
-#ifndef PACO_STAGE
         // head of the next decision's dependent chain, issued before any bookkeeping
         e_pre = ldg_u64_if(row_base + (size_t)next * kp, lane_in, make_uint2(next, 0u));
-#endif
+        // off-chain bookkeeping overlapping the load: the visit of next (one lane,
+        // fire-and-forget; no candidate of next is next itself), the tour entry and the
+        // next decision's draw word
         red_or_shared_if(vis_s + ((next >> 5) << 2), 1u << (next & 31), lane == 0);
         stg_u32_if(out + pos, next, lane == 0);
         ++pos;
@@ -649,14 +637,23 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     cp_async_wait_all();
     __syncwarp();
 #ifdef PACO_TIMING
-    if (lane == 0) { atomicAdd(&g_timing[0], (unsigned long long)(clock64() - loop0)); atomicAdd(&g_timing[2], (unsigned long long)n_dec);
+    if (lane == 0) {
+        atomicAdd(&g_timing[0], (unsigned long long)(clock64() - loop0));
         atomicAdd(&g_timing[1], (unsigned long long)fbc);
+        atomicAdd(&g_timing[2], (unsigned long long)n_dec);
         atomicAdd(&g_timing[4], (unsigned long long)seg0); atomicAdd(&g_timing[5], (unsigned long long)seg1);
         atomicAdd(&g_timing[6], (unsigned long long)seg2); atomicAdd(&g_timing[7], (unsigned long long)segn);
-        atomicAdd(&g_timing[3], (unsigned long long)segw); atomicAdd(&g_timing[8], (unsigned long long)sege); }
-    { long long c = fs.cities; for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-      if (lane == 0) { atomicAdd(&g_timing[9], (unsigned long long)fs.searches); atomicAdd(&g_timing[10], (unsigned long long)fs.rings);
-        atomicAdd(&g_timing[11], (unsigned long long)fs.sbs); atomicAdd(&g_timing[12], (unsigned long long)c); } }
+    }
+    {
+        long long c = fs.cities;
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+        if (lane == 0) {
+            atomicAdd(&g_timing[9], (unsigned long long)fs.searches); atomicAdd(&g_timing[10], (unsigned long long)fs.rings);
+            atomicAdd(&g_timing[11], (unsigned long long)fs.sbs); atomicAdd(&g_timing[12], (unsigned long long)c);
+            atomicAdd(&g_timing[13], (unsigned long long)fs.t_test); atomicAdd(&g_timing[14], (unsigned long long)fs.t_scan);
+            atomicAdd(&g_timing[15], (unsigned long long)fs.t_argmin); atomicAdd(&g_timing[3], (unsigned long long)fs.t_pre);
+        }
+    }
 #endif
     // tour length (instance.hpp:120-127), int64, warp-parallel over positions
     long long len = 0;

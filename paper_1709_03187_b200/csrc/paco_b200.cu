@@ -340,7 +340,7 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
     const uint32_t kk = std::min<uint32_t>(cfg->candidates, n - 1), kpp = (kk + 1) & ~1u;
     (void)kpp;
     const bool ir = cfg->rule == PACO_RULE_INDEPENDENT_ROULETTE;
-    const size_t smem_need = ir ? ir_smem_bytes(n, nwords, mode) : 512 + (size_t)nwords * 4;
+    const size_t smem_need = ir ? ir_smem_bytes(n, nwords, mode) : kFbList * 4 + (size_t)nwords * 4;
     if (smem_need > (size_t)prop.sharedMemPerBlockOptin)
         return fail(PACO_E_UNSUPPORTED, ir ? "reference-rule per-ant state exceeds shared memory (n too large)"
                                            : "visited bitmap exceeds shared memory (n too large)");
@@ -440,11 +440,7 @@ static ConstructArgs construct_args(paco_handle* h, bool seeding) {
 
 static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint32_t blocks) {
     // shared memory: double-buffered stage of k candidate rows + the n-bit visited bitmap
-#ifdef PACO_STAGE
-    const size_t smem = (size_t)2 * h->k * h->kp * 8 + (size_t)h->nwords * 4;
-#else
-    const size_t smem = 512 + (size_t)h->nwords * 4;
-#endif
+    const size_t smem = kFbList * 4 + (size_t)h->nwords * 4 + 512 + 16;  // fallback list + visited bitmap + scratch
     const bool buf = a.words != nullptr;
     // Shared-memory carveout: just enough for the CTAs one SM must host to run every ant at
     // once (ceil(m / #SMs) warps), so the rest of the unified L1 caches candidate rows.
