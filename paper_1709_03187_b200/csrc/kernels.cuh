@@ -295,7 +295,22 @@ constexpr uint32_t kFbList = 256;  // per-warp shared-memory list of unvisited c
 //     scored with one coordinate load per lane — one L2 round trip per ring instead of
 //     one per superblock. Original indices (the tie-break key) are loaded only on an
 //     exact distance tie and once per lane before the per-ring warp argmin.
-__device__ __forceinline__ uint32_t nearest_unvisited(const ConstructArgs& a, const uint32_t* vis, uint32_t cur,
+// Everything the fallback reads, kept in shared memory so the (rarely executed)
+// fallback can be a separate function without an argument struct on the stack.
+struct FallbackCtx {
+    const uint32_t* knn32;
+    const double2* xy;
+    const uint32_t* orig_of;
+    const uint32_t* cell_start;
+    GridParams g;
+};
+
+#ifdef PACO_FB_INLINE
+#define PACO_FB_ATTR __forceinline__
+#else
+#define PACO_FB_ATTR __noinline__
+#endif
+__device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const uint32_t* vis, uint32_t cur,
                                                    uint32_t lane, uint32_t* list, FbStats& fs) {
     {
         const uint32_t c = ldg_u32(&a.knn32[(size_t)cur * 32 + lane]);
@@ -398,8 +413,7 @@ __device__ __forceinline__ uint32_t nearest_unvisited(const ConstructArgs& a, co
 #ifdef PACO_TIMING
         long long ta0 = clock64();
 #endif
-        if (bo == kNone && bj != kNone) bo = a.orig_of[bj];
-        warp_argmin(bd, bo, bj);
+        warp_argmin_lazy(bd, bo, bj, a.orig_of, lane);
 #ifdef PACO_TIMING
         { long long ta1; asm volatile("mov.u64 %0, %%clock64;" : "=l"(ta1) : "r"(bj)); fs.t_argmin += ta1 - ta0; }
 #endif
@@ -483,6 +497,8 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
         const uint4 v = philox10(make_uint4(slot >> 2, ant, (uint32_t)a.iter, (uint32_t)(a.iter >> 32)), key);
         return pick_word(v, slot & 3);
     };
+    __shared__ FallbackCtx fctx;
+    if (lane == 0) { fctx.knn32 = a.knn32; fctx.xy = a.xy; fctx.orig_of = a.orig_of; fctx.cell_start = a.cell_start; fctx.g = a.g; }
     for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
     __syncwarp();
     if (lane == 0 && (n & 31)) vis[nw - 1] = 0xffffffffu << (n & 31);  // padding bits count as visited
@@ -606,7 +622,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
 #ifdef PACO_TIMING
                 const long long c0 = clock64();
 #endif
-                next = nearest_unvisited(a, vis, cur, lane, fb_list, fs);
+                next = nearest_unvisited(fctx, vis, cur, lane, fb_list, fs);
 #ifdef PACO_TIMING
                 fbc += clock64() - c0;
 #endif
