@@ -59,8 +59,8 @@ typedef struct paco_config {
     double alpha, beta;
     double partial_prob;           /* engine.hpp:47 */
     double max_mod_frac;           /* engine.hpp:48 */
-    double two_opt_prob;           /* engine.hpp:49 -- only 0 is supported (PACO_E_UNSUPPORTED) */
-    uint32_t two_opt_window;
+    double two_opt_prob;           /* engine.hpp:49, first-improvement 2-opt after construction */
+    uint32_t two_opt_window;       /* engine.hpp:50, 0 = unbounded (two_opt.hpp:33-35) */
     uint32_t synchronous;          /* must be 1: the GPU engine is the barrier-sync path */
     uint64_t seed;
     double rho, tau_max, tau0;
@@ -84,6 +84,7 @@ typedef struct paco_counters {
     uint64_t iterations;
     uint64_t improvements;   /* successful update_l_best calls */
     uint64_t comparisons;    /* candidate scores evaluated (IR rule: the reference's comparison count) */
+    uint64_t two_opts;       /* constructions that ran 2-opt (maybe_two_opt, two_opt.hpp:71-76) */
 } paco_counters;
 
 /* RunReport, engine.hpp:84-92 (+ counters and device-time breakdown) */

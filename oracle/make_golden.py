@@ -97,18 +97,35 @@ def main() -> None:
     g.update(classic_tours=ct, classic_lens=cl, classic_rho=np.float64(0.5), classic_tau=np.float64(1.0))
     g["classic_ref"] = oracle.ref_classic_update(n, 0.5, 1.0, ct, cl)
 
+    # --- first-improvement 2-opt (two_opt.hpp:28-67): KAT square + random tours, windows
+    sq_x = np.array([0.0, 10.0, 10.0, 0.0]); sq_y = np.array([0.0, 0.0, 10.0, 10.0])
+    g["twoopt_sq"] = oracle.ref_two_opt(sq_x, sq_y, np.array([0, 2, 1, 3], np.uint32))[0]
+    tcases = []
+    for ti, (n, window) in enumerate([(9, 0), (25, 0), (60, 0), (60, 5), (120, 16), (200, 0)]):
+        x = rng.integers(0, 1000, n).astype(np.float64)
+        y = rng.integers(0, 1000, n).astype(np.float64)
+        order = rng.permutation(n).astype(np.uint32)
+        out, ln = oracle.ref_two_opt(x, y, order, window)
+        g.update({f"twoopt{ti}_x": x, f"twoopt{ti}_y": y, f"twoopt{ti}_in": order, f"twoopt{ti}_out": out,
+                  f"twoopt{ti}_len": np.int64(ln), f"twoopt{ti}_window": np.uint32(window)})
+        tcases.append(ti)
+    g["twoopt_cases"] = np.array(tcases)
+
     # --- Rng::for_stream (rng.hpp:33-50) raw outputs, for the IR-rule mode
     g["stream_ref"] = np.stack([oracle.ref_stream_u64(7, s, 64) for s in range(4)])
 
     # --- whole-run reference results (IR rule, sync mode) on small instances
     runs = []
-    for ri, (n, m, iters, mode) in enumerate([(12, 4, 30, "partial"), (30, 8, 20, "paco"), (25, 6, 10, "classic")]):
+    for ri, (n, m, iters, mode, p2, w2) in enumerate([(12, 4, 30, "partial", 0.0, 0), (30, 8, 20, "paco", 0.0, 0),
+                                                      (25, 6, 10, "classic", 0.0, 0), (40, 6, 25, "partial", 0.3, 0),
+                                                      (80, 8, 15, "partial", 0.05, 10)]):
         x = rng.integers(0, 1000, n).astype(np.float64)
         y = rng.integers(0, 1000, n).astype(np.float64)
         r = oracle.ref_run(x, y, ants=m, iterations=iters, alpha=1.0, beta=2.0, seed=11 + ri, mode=mode,
-                           workers=2, rho=0.5)
+                           workers=2, rho=0.5, two_opt_prob=p2, two_opt_window=w2)
         g[f"run{ri}_x"], g[f"run{ri}_y"] = x, y
         g[f"run{ri}_cfg"] = np.array([n, m, iters, ["partial", "paco", "classic"].index(mode), 11 + ri])
+        g[f"run{ri}_twoopt"] = np.array([p2, w2], dtype=np.float64)
         g[f"run{ri}_best"] = np.int64(r["best_length"])
         g[f"run{ri}_tour"] = r["best_tour"]
         g[f"run{ri}_comparisons"] = np.uint64(r["comparisons"])

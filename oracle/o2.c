@@ -79,6 +79,39 @@ static inline double d2_of(const double* xs, const double* ys, uint32_t i, uint3
     return dx * dx + dy * dy;
 }
 
+/* two_opt_scan (two_opt.hpp:28-51): first improving reversal in lexicographic (i, j)
+ * order, window bounds j - i on the linear order; returns the length delta (0 = none). */
+static int64_t two_opt_scan(const double* xs, const double* ys, uint32_t n, uint32_t* o, uint32_t window) {
+#define D(p, q) ((int64_t)o2_euc2d(xs[p], ys[p], xs[q], ys[q]))
+    for (uint32_t i = 0; i + 1 < n; ++i) {
+        const uint32_t a = o[i], b = o[i + 1];
+        const int64_t d_ab = D(a, b);
+        const uint32_t j_end = window == 0 ? n - 1 : (n - 1 < i + window ? n - 1 : i + window);
+        for (uint32_t j = i + 1; j <= j_end; ++j) {
+            if (i == 0 && j == n - 1) continue;
+            const uint32_t c = o[j], d = o[(j + 1) % n];
+            const int64_t before = d_ab + D(c, d), after = D(a, c) + D(b, d);
+            if (after < before) {
+                for (uint32_t l = i + 1, r = j; l < r; ++l, --r) { const uint32_t t = o[l]; o[l] = o[r]; o[r] = t; }
+                return after - before;
+            }
+        }
+    }
+    return 0;
+#undef D
+}
+
+/* two_opt (two_opt.hpp:58-67): restart the scan after every accepted move */
+int64_t o2_two_opt(const double* xs, const double* ys, uint32_t n, uint32_t* order, uint32_t window) {
+    int64_t total = 0;
+    for (;;) {
+        const int64_t d = two_opt_scan(xs, ys, n, order, window);
+        if (d == 0) break;
+        total += d;
+    }
+    return total;
+}
+
 /* top-k by (d^2, index) -- brute force over all j != i */
 static void knn_row(const double* xs, const double* ys, uint32_t n, uint32_t k, uint32_t i,
                     uint32_t* out, double* kd) {
@@ -314,6 +347,10 @@ static int build_one(o2_state* s, uint32_t ant, int seeding, const uint32_t* wor
     if (err) return -1;
     s->partial_flag[ant] = (uint8_t)partial;
     if (complete_tour(s, ant, order, pos, vis, words, stride, c)) return -1;
+    /* maybe_two_opt (two_opt.hpp:71-76): draw slot 3 */
+    const double u2 = u01_f64(word_of(s, ant, 3, words, stride, &err));
+    if (err) return -1;
+    if (u2 < s->p.two_opt_prob) { o2_two_opt(s->xs, s->ys, n, order, s->p.two_opt_window); c->two_opts++; }
     s->lens[ant] = o2_cycle_length(s->xs, s->ys, n, order);
     return 0;
 }
@@ -383,6 +420,7 @@ static int par_for(o2_state* s, int kind, uint32_t total, const double* ratios, 
         s->cnt.decisions += jobs[t].c.decisions; s->cnt.fallbacks += jobs[t].c.fallbacks;
         s->cnt.ties += jobs[t].c.ties; s->cnt.forced += jobs[t].c.forced;
         s->cnt.full_builds += jobs[t].c.full_builds; s->cnt.partial_builds += jobs[t].c.partial_builds;
+        s->cnt.two_opts += jobs[t].c.two_opts;
     }
     free(jobs); free(th);
     return rc;

@@ -16,6 +16,7 @@
  *   - sync completion step, strict l/g update  proj/include/paco/engine.hpp:245-306,
  *                                              proj/include/paco/colony.hpp:115-139
  *   - classic evaporate/deposit (edge-local)   proj/include/paco/construction.hpp:187-207
+ *   - first-improvement (windowed) 2-opt       proj/include/paco/two_opt.hpp:28-76
  * North-star additions (no reference code; defined in DESIGN.md §3):
  *   - k-NN candidate lists ordered by (d^2, original index)
  *   - roulette over the list: f32 weights, 32-lane Hillis-Steele inclusive scan
@@ -39,6 +40,9 @@ typedef struct o2_params {
     uint32_t n, m, k;
     uint32_t threads;
     double alpha, beta, tau0, partial_prob, max_mod_frac, rho, tau_max;
+    double two_opt_prob;     /* maybe_two_opt (two_opt.hpp:71-76), draw slot 3 */
+    uint32_t two_opt_window; /* 0 = unbounded */
+    uint32_t pad2_;
     uint64_t seed;
     int32_t mode;           /* 0 partial, 1 paco (always full), 2 classic */
     int32_t draw_source;    /* 0 philox, 1 caller buffer per iteration */
@@ -47,7 +51,7 @@ typedef struct o2_params {
 } o2_params;
 
 typedef struct o2_counters {
-    uint64_t decisions, fallbacks, ties, forced, full_builds, partial_builds, iterations;
+    uint64_t decisions, fallbacks, ties, forced, full_builds, partial_builds, iterations, two_opts;
 } o2_counters;
 
 typedef struct o2_state o2_state;
@@ -58,6 +62,8 @@ uint32_t o2_draw_word(uint64_t seed, uint32_t ant, uint64_t iter, uint32_t slot)
 int32_t o2_euc2d(double x1, double y1, double x2, double y2);
 double o2_power(double e, double x);
 int64_t o2_cycle_length(const double* xs, const double* ys, uint32_t n, const uint32_t* order);
+/* first-improvement 2-opt to a local optimum (two_opt.hpp:28-67); returns the length delta */
+int64_t o2_two_opt(const double* xs, const double* ys, uint32_t n, uint32_t* order, uint32_t window);
 void o2_knn_brute(const double* xs, const double* ys, uint32_t n, uint32_t k, uint32_t* out);
 void o2_knn_rows(const double* xs, const double* ys, uint32_t n, uint32_t k,
                  const uint32_t* rows, uint32_t nrows, uint32_t* out);

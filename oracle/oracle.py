@@ -30,13 +30,14 @@ def build(ref: bool = True) -> None:
 class O2Params(ctypes.Structure):
     _fields_ = [("n", c_uint32), ("m", c_uint32), ("k", c_uint32), ("threads", c_uint32),
                 ("alpha", c_double), ("beta", c_double), ("tau0", c_double), ("partial_prob", c_double),
-                ("max_mod_frac", c_double), ("rho", c_double), ("tau_max", c_double), ("seed", c_uint64),
+                ("max_mod_frac", c_double), ("rho", c_double), ("tau_max", c_double), ("two_opt_prob", c_double),
+                ("two_opt_window", c_uint32), ("pad2_", c_uint32), ("seed", c_uint64),
                 ("mode", c_int32), ("draw_source", c_int32), ("fallback_brute", c_int32), ("pad_", c_int32)]
 
 
 class O2Counters(ctypes.Structure):
     _fields_ = [(f, c_uint64) for f in ("decisions", "fallbacks", "ties", "forced", "full_builds",
-                                        "partial_builds", "iterations")]
+                                        "partial_builds", "iterations", "two_opts")]
 
 
 def _p(a, t):
@@ -78,6 +79,8 @@ def o2lib():
         L.o2_euc2d.argtypes = [c_double] * 4
         L.o2_power.restype = c_double
         L.o2_power.argtypes = [c_double, c_double]
+        L.o2_two_opt.restype = c_int64
+        L.o2_two_opt.argtypes = [POINTER(c_double), POINTER(c_double), c_uint32, POINTER(c_uint32), c_uint32]
         L.o2_cycle_length.restype = c_int64
         L.o2_cycle_length.argtypes = [POINTER(c_double), POINTER(c_double), c_uint32, POINTER(c_uint32)]
         L.o2_knn_brute.argtypes = [POINTER(c_double), POINTER(c_double), c_uint32, c_uint32, POINTER(c_uint32)]
@@ -98,7 +101,7 @@ class O2:
 
     def __init__(self, xs, ys, m, k, alpha=1.0, beta=2.0, tau0=1.0, partial_prob=0.95, max_mod_frac=1.0,
                  rho=0.5, tau_max=1.0, seed=1, mode="partial", draws="philox", threads=None,
-                 fallback_brute=False):
+                 fallback_brute=False, two_opt_prob=0.0, two_opt_window=0):
         self.L = o2lib()
         self.xs = np.ascontiguousarray(xs, np.float64)
         self.ys = np.ascontiguousarray(ys, np.float64)
@@ -106,7 +109,7 @@ class O2:
         self.k = min(k, self.n - 1, 32)
         p = O2Params(n=self.n, m=m, k=k, threads=threads or os.cpu_count() or 1, alpha=alpha, beta=beta,
                      tau0=tau0, partial_prob=partial_prob, max_mod_frac=max_mod_frac, rho=rho, tau_max=tau_max,
-                     seed=seed, mode=MODES[mode], draw_source=1 if draws == "buffer" else 0,
+                     two_opt_prob=two_opt_prob, two_opt_window=two_opt_window, seed=seed, mode=MODES[mode], draw_source=1 if draws == "buffer" else 0,
                      fallback_brute=1 if fallback_brute else 0)
         self.h = self.L.o2_create(_p(self.xs, c_double), _p(self.ys, c_double), ctypes.byref(p))
         if not self.h:
@@ -287,6 +290,8 @@ def reflib():
                                          POINTER(c_uint32), POINTER(c_uint32), c_uint32, POINTER(c_uint8),
                                          POINTER(c_int64)]
         L.ref_stream_u64.argtypes = [c_uint64, c_uint64, c_uint64, POINTER(c_uint64)]
+        L.ref_two_opt.argtypes = [POINTER(c_double), POINTER(c_double), c_uint32, POINTER(c_uint32), c_uint32,
+                                  POINTER(c_uint32), POINTER(c_int64)]
         L.ref_classic_update.argtypes = [c_uint32, c_double, c_double, POINTER(c_uint32), POINTER(c_int64),
                                          c_uint32, c_uint32, POINTER(c_double)]
         L.ref_run.argtypes = [POINTER(c_double), POINTER(c_double), c_uint32, POINTER(RefRunParams),
@@ -299,14 +304,24 @@ def reflib():
     return _ref
 
 
+def two_opt(xs, ys, order, window=0):
+    xs = np.ascontiguousarray(xs, np.float64)
+    ys = np.ascontiguousarray(ys, np.float64)
+    o = np.array(order, dtype=np.uint32)
+    d = o2lib().o2_two_opt(_p(xs, c_double), _p(ys, c_double), xs.size, _p(o, c_uint32), window)
+    return o, int(d)
+
+
 def ref_run(xs, ys, ants, iterations, alpha, beta, seed=1, mode="partial", workers=None, partial_prob=0.95,
-            max_mod_frac=1.0, rho=0.1, tau_max=1.0, tau0=1.0, synchronous=True, time_budget_s=0.0):
+            max_mod_frac=1.0, rho=0.1, tau_max=1.0, tau0=1.0, synchronous=True, time_budget_s=0.0,
+            two_opt_prob=0.0, two_opt_window=0):
     L = reflib()
     xs = np.ascontiguousarray(xs, np.float64)
     ys = np.ascontiguousarray(ys, np.float64)
     p = RefRunParams(ants=ants, workers=workers or os.cpu_count() or 1, iterations=iterations, seed=seed,
                      alpha=alpha, beta=beta, partial_prob=partial_prob, max_mod_frac=max_mod_frac,
-                     two_opt_prob=0.0, two_opt_window=0, synchronous=1 if synchronous else 0, rho=rho,
+                     two_opt_prob=two_opt_prob, two_opt_window=two_opt_window, synchronous=1 if synchronous else 0,
+                     rho=rho,
                      tau_max=tau_max, tau0=tau0, time_budget_s=time_budget_s, mode=MODES[mode])
     best = c_int64()
     tour = np.empty(xs.size, np.uint32)
@@ -408,3 +423,17 @@ def ref_stream_u64(seed, stream, count):
     out = np.empty(count, np.uint64)
     reflib().ref_stream_u64(seed, stream, count, _p(out, c_uint64))
     return out
+
+
+def ref_two_opt(xs, ys, order, window=0):
+    L = reflib()
+    xs = np.ascontiguousarray(xs, np.float64)
+    ys = np.ascontiguousarray(ys, np.float64)
+    o = np.ascontiguousarray(order, np.uint32)
+    out = np.empty(o.size, np.uint32)
+    ln = c_int64()
+    rc = L.ref_two_opt(_p(xs, c_double), _p(ys, c_double), xs.size, _p(o, c_uint32), window, _p(out, c_uint32),
+                       ctypes.byref(ln))
+    if rc:
+        raise RuntimeError(L.ref_last_error().decode())
+    return out, ln.value

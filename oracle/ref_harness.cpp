@@ -18,6 +18,7 @@
 #include "paco/engine.hpp"
 #include "paco/instance.hpp"
 #include "paco/rng.hpp"
+#include "paco/two_opt.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -118,6 +119,19 @@ int ref_offer_sequence(const double* xs, const double* ys, uint32_t n, uint32_t 
             flags[q] = imp ? 1 : 0;
             g_after[q] = colony.g_best_length();
         }
+    });
+}
+
+// two_opt (two_opt.hpp:58-67) on a given order; returns the new order and length.
+int ref_two_opt(const double* xs, const double* ys, uint32_t n, const uint32_t* order, uint32_t window,
+                uint32_t* out, int64_t* length) {
+    return guarded([&] {
+        const auto inst = make_instance(xs, ys, n);
+        paco::Tour t = paco::make_tour(inst, std::vector<uint32_t>(order, order + n));
+        paco::TwoOptParams prm{1.0, window};
+        const paco::Tour r = paco::two_opt(inst, t, prm);
+        std::memcpy(out, r.order.data(), sizeof(uint32_t) * n);
+        *length = r.length;
     });
 }
 

@@ -47,7 +47,7 @@ class Config(ctypes.Structure):
 class Counters(ctypes.Structure):
     _fields_ = [(name, c_uint64) for name in (
         "decisions", "fallbacks", "ties", "forced", "full_builds", "partial_builds", "iterations",
-        "improvements", "comparisons")]
+        "improvements", "comparisons", "two_opts")]
 
     def as_dict(self) -> dict:
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

@@ -265,6 +265,8 @@ struct ConstructArgs {
     int validate;
     int* err;
     // explicit construct_partial_at (tests): ant = force_ant, params given
+    double two_opt_prob;       // maybe_two_opt (two_opt.hpp:71-76), draw slot 3
+    uint32_t two_opt_window;
     int force;
     uint32_t force_ant, force_start_pos, force_m_mod;
 };
@@ -671,6 +673,12 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
         }
     }
 #endif
+    // maybe_two_opt (two_opt.hpp:71-76): draw slot 3
+    uint32_t n_2opt = 0;
+    if (!a.force && a.two_opt_prob > 0.0 && u01_f64(word(3)) < a.two_opt_prob) {
+        two_opt_warp(out, n, a.two_opt_window, a.xy, lane);
+        n_2opt = 1;
+    }
     // tour length (instance.hpp:120-127), int64, warp-parallel over positions
     long long len = 0;
     for (uint32_t p = lane; p < n; p += 32) {
@@ -701,6 +709,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
             atomicAdd(&a.counters[2], (unsigned long long)n_tie);
             atomicAdd(&a.counters[3], (unsigned long long)n_forced);
             atomicAdd(&a.counters[partial ? 5 : 4], 1ull);
+            if (n_2opt) atomicAdd(&a.counters[9], 1ull);
         }
     }
 }

@@ -53,6 +53,8 @@ struct IrArgs {
     uint32_t n, m, nwords;
     double alpha, beta, tau0, eff_pp, mmf;
     int seeding, coin_always, eta_table;  // eta_table: reference table path (n <= 5000) rounds eta^beta to f32
+    double two_opt_prob;
+    uint32_t two_opt_window;
 };
 
 // One warp per ant: detail::build_candidate (engine.hpp:129-148) with construct_full /
@@ -210,9 +212,12 @@ __global__ void __launch_bounds__(32, 1) k_construct_ir(IrArgs a) {
         ++pos;
         cur = next;
     }
-    // maybe_two_opt consumes exactly one draw (two_opt.hpp:71-76); 2-opt itself is off
-    if (lane == 0) (void)xo_uniform(s);
+    // maybe_two_opt consumes exactly one draw (two_opt.hpp:71-76)
+    uint32_t do2 = 0;
+    if (lane == 0) do2 = xo_uniform(s) < a.two_opt_prob ? 1u : 0u;
+    do2 = __shfl_sync(kFull, do2, 0);
     __syncwarp();
+    if (do2) two_opt_warp(out, n, a.two_opt_window, a.xy, lane);
     long long len = 0;
     for (uint32_t p = lane; p < n; p += 32) len += euc2d(a.xy[out[p]], a.xy[out[p + 1 < n ? p + 1 : 0]]);
 #pragma unroll
@@ -225,6 +230,7 @@ __global__ void __launch_bounds__(32, 1) k_construct_ir(IrArgs a) {
         atomicAdd(&a.counters[3], n_forced);
         atomicAdd(&a.counters[partial ? 5 : 4], 1ull);
         atomicAdd(&a.counters[8], n_cmp);
+        if (do2) atomicAdd(&a.counters[9], 1ull);
     }
 }
 

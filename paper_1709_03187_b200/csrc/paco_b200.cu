@@ -144,7 +144,6 @@ paco_status paco_config_validate(const paco_config* c, uint32_t n, int mode) {
     if (c->rule > 1) return fail(PACO_E_INVALID, "unknown selection rule");
     if (c->rule == PACO_RULE_INDEPENDENT_ROULETTE && c->draws != PACO_DRAWS_PHILOX)
         return fail(PACO_E_INVALID, "the reference rule draws from its own xoshiro256++ streams");
-    if (c->two_opt_prob > 0.0) return fail(PACO_E_UNSUPPORTED, "2-opt is not provided by the GPU engine yet");
     if (!c->synchronous) return fail(PACO_E_UNSUPPORTED, "asynchronous mode is not provided by the GPU engine yet");
     return PACO_OK;
 }
@@ -414,6 +413,7 @@ static paco_status launch_construct_ir(paco_handle* h, bool seeding) {
     a.seeding = seeding ? 1 : 0;
     a.coin_always = 0;
     a.eta_table = h->n <= 5000 ? 1 : 0;  // Heuristic keeps an f32 table iff the instance has a matrix
+    a.two_opt_prob = h->cfg.two_opt_prob; a.two_opt_window = h->cfg.two_opt_window;
     const size_t smem = ir_smem_bytes(h->n, h->nwords, h->mode);
     if (smem > 48 * 1024)
         CU(cudaFuncSetAttribute(k_construct_ir, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -435,6 +435,7 @@ static ConstructArgs construct_args(paco_handle* h, bool seeding) {
     a.seeding = seeding ? 1 : 0;
     a.validate = h->cfg.validate_tours ? 1 : 0;
     a.err = h->err;
+    a.two_opt_prob = h->cfg.two_opt_prob; a.two_opt_window = h->cfg.two_opt_window;
     return a;
 }
 
@@ -616,6 +617,7 @@ paco_status paco_get_counters(paco_handle* h, paco_counters* c) {
     c->decisions = v[0]; c->fallbacks = v[1]; c->ties = v[2]; c->forced = v[3];
     c->full_builds = v[4]; c->partial_builds = v[5]; c->iterations = h->iter; c->improvements = v[7];
     c->comparisons = h->ir ? v[8] : v[0];
+    c->two_opts = v[9];
     return PACO_OK;
 }
 

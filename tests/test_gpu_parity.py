@@ -24,10 +24,12 @@ def lockstep(inst, iters, mode=Mode.partial_aco, words_fn=None, check_every=1, *
     cfg = RunConfig(ants=m, iterations=iters, alpha=kw.get("alpha", 1.0), beta=kw.get("beta", 2.0),
                     rho=kw.get("rho", 0.5), tau0=kw.get("tau0", 1.0), partial_prob=kw.get("partial_prob", 0.95),
                     max_mod_frac=kw.get("max_mod_frac", 1.0), seed=kw.get("seed", 1), candidates=k,
-                    draws="buffer" if words_fn else "philox", validate_tours=True)
+                    draws="buffer" if words_fn else "philox", validate_tours=True,
+                    two_opt_prob=kw.get("two_opt_prob", 0.0), two_opt_window=kw.get("two_opt_window", 0))
     ref = oracle.O2(inst.xs, inst.ys, m=m, k=k, alpha=cfg.alpha, beta=cfg.beta, tau0=cfg.tau0,
                     partial_prob=cfg.partial_prob, max_mod_frac=cfg.max_mod_frac, rho=cfg.rho, seed=cfg.seed,
-                    mode=MODE_NAMES[mode], draws="buffer" if words_fn else "philox")
+                    mode=MODE_NAMES[mode], draws="buffer" if words_fn else "philox",
+                    two_opt_prob=cfg.two_opt_prob, two_opt_window=cfg.two_opt_window)
     col = Colony(inst, cfg, mode)
     knn_gpu, _ = col.candidates()
     assert np.array_equal(knn_gpu, ref.knn()), "k-NN candidate lists differ"
@@ -63,7 +65,7 @@ def lockstep(inst, iters, mode=Mode.partial_aco, words_fn=None, check_every=1, *
             assert gl <= g_prev
         g_prev = gl
     cg, cr = col.counters(), ref.counters()
-    for key in ("decisions", "fallbacks", "ties", "forced", "full_builds", "partial_builds"):
+    for key in ("decisions", "fallbacks", "ties", "forced", "full_builds", "partial_builds", "two_opts"):
         assert cg[key] == cr[key], (key, cg[key], cr[key])
     return col, ref
 
@@ -95,6 +97,15 @@ def test_paco_and_small_cap_modes():
 def test_classic_mode():
     inst = make_config_instance("C1", n=800)
     col, ref = lockstep(inst, 12, mode=Mode.classic_aco, ants=20, candidates=20, rho=0.5)
+
+
+@pytest.mark.parametrize("p2,w2", [(0.25, 0), (0.5, 12)])
+def test_two_opt_after_construction(p2, w2):
+    """maybe_two_opt (two_opt.hpp:71-76) on the north-star rule: draw slot 3, first-improvement
+    2-opt (windowed or not) on the built tour, identical to O2."""
+    inst = make_config_instance("C1", n=250)
+    col, ref = lockstep(inst, 8, ants=12, candidates=10, two_opt_prob=p2, two_opt_window=w2, seed=6)
+    assert col.counters()["two_opts"] == ref.counters()["two_opts"] > 0
 
 
 def test_validation_buffer_draws():
@@ -227,7 +238,7 @@ def test_config_errors():
     with pytest.raises(InvalidArgument):
         Colony(inst, RunConfig(ants=0))
     with pytest.raises(PacoError):
-        Colony(inst, RunConfig(ants=4, two_opt_prob=0.1))
+        Colony(inst, RunConfig(ants=4, synchronous=False))
 
 
 def test_cpp_drop_in_on_gpu(tmp_path):

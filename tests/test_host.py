@@ -155,8 +155,9 @@ def test_classic_size_limit_and_unsupported(native):
     with pytest.raises(InvalidArgument, match="classic mode requires n <= 5000"):
         RunConfig().validate(n=5001, mode=Mode.classic_aco)
     RunConfig().validate(n=5000, mode=Mode.classic_aco)
+    RunConfig(two_opt_prob=0.1, two_opt_window=500).validate()  # f2: supported
     with pytest.raises(PacoError) as ei:
-        RunConfig(two_opt_prob=0.1).validate()
+        RunConfig(synchronous=False).validate()
     assert ei.value.status == N.PACO_E_UNSUPPORTED
 
 

@@ -268,3 +268,17 @@ def test_live_reference_colony_random():
             o.offer_tour(a, tours[a])
         for i in range(n):
             assert np.array_equal(o.tau_row(i), ref[i])
+
+
+def test_two_opt_matches_reference():
+    """two_opt (two_opt.hpp:28-67): the square KAT of test_two_opt.cpp:11-21 (48 -> 40) and random
+    tours with and without a window, move sequence identical to the reference."""
+    assert list(GOLD["twoopt_sq"]) == [0, 1, 2, 3]
+    sq_x = np.array([0.0, 10.0, 10.0, 0.0]); sq_y = np.array([0.0, 0.0, 10.0, 10.0])
+    o, d = oracle.two_opt(sq_x, sq_y, [0, 2, 1, 3])
+    assert d == -8 and list(o) == [0, 1, 2, 3]
+    for ti in GOLD["twoopt_cases"]:
+        x, y = GOLD[f"twoopt{ti}_x"], GOLD[f"twoopt{ti}_y"]
+        o, d = oracle.two_opt(x, y, GOLD[f"twoopt{ti}_in"], int(GOLD[f"twoopt{ti}_window"]))
+        assert np.array_equal(o, GOLD[f"twoopt{ti}_out"])
+        assert oracle.cycle_length(x, y, o) == int(GOLD[f"twoopt{ti}_len"])
