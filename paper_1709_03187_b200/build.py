@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libpaco_b200.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("paco_b200.cu",)]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "device.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "kernels_ir.cuh", "device.cuh")] + [
     os.path.join(ROOT, "include", "paco_b200.h")]
 
 NVCC_FLAGS = [

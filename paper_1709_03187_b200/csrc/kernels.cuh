@@ -6,6 +6,7 @@
 namespace pacob200 {
 #ifdef PACO_TIMING
 __device__ unsigned long long g_timing[16];
+__device__ unsigned long long g_prof[96];  // ant 0 profile by tour position (20 buckets)
 #endif
 
 // ============================================================ K0: spatial sort
@@ -44,6 +45,12 @@ __global__ void k_cell_start(const uint32_t* __restrict__ cellm, uint32_t n, uin
         for (uint32_t q = lo; q <= c; ++q) cell_start[q] = p;
     if (p == n - 1)
         for (uint32_t q = c + 1; q <= ncells; ++q) cell_start[q] = n;
+}
+
+// sb_start[b] = first internal id of Morton superblock b (8x8 cells = 64 Morton codes)
+__global__ void k_sb_start(const uint32_t* __restrict__ cell_start, uint32_t nsb, uint32_t* __restrict__ sb_start) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b <= nsb) sb_start[b] = cell_start[(size_t)b << 6];
 }
 
 // ============================================================ K1: k-NN lists
@@ -249,7 +256,7 @@ struct ConstructArgs {
     const double2* xy;        // internal coordinates
     const uint32_t* orig_of;  // internal -> original (fallback tie-break)
     const uint32_t* int_of;   // original -> internal (start city draw)
-    const uint32_t* cell_start;
+    const uint32_t* sb_start;   // first internal id of every Morton superblock
     GridParams g;
     uint32_t* tours;          // m * 2 * n; l_best in half lb_sel[a], new tour in the other
     const uint8_t* lb_sel;
@@ -287,31 +294,67 @@ struct FbStats {
 
 constexpr uint32_t kFbList = 256;  // per-warp shared-memory list of unvisited city ids (fallback)
 
-// Exact nearest unvisited city by (d^2, original index), warp-cooperative.
-// F0: the 32-nearest list is sorted by the same key, so its first unvisited entry
-//     is the answer whenever one exists (one 128-byte row, one ballot).
-// F1: rings of 8x8-cell superblocks (each a contiguous id range) around cur with
-//     squared rectangle lower bounds. Per ring pass, each lane takes one superblock,
-//     counts its unvisited cities from the shared-memory bitmap, a warp scan turns the
-//     counts into offsets, the ids are appended to a shared list and the whole list is
-//     scored with one coordinate load per lane — one L2 round trip per ring instead of
-//     one per superblock. Original indices (the tie-break key) are loaded only on an
-//     exact distance tie and once per lane before the per-ring warp argmin.
 // Everything the fallback reads, kept in shared memory so the (rarely executed)
 // fallback can be a separate function without an argument struct on the stack.
 struct FallbackCtx {
     const uint32_t* knn32;
     const double2* xy;
     const uint32_t* orig_of;
-    const uint32_t* cell_start;
+    const uint32_t* sb_start;  // first internal id of every Morton superblock (+ end sentinel)
     GridParams g;
 };
+
+__device__ __forceinline__ double2 ldg_d2(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+// Warp argmin by (d^2, original index). Non-negative doubles order like their bit
+// patterns, so the distance minimum is two integer min-reductions (high word, then low
+// word among the lanes holding the high minimum). Original indices are fetched only if
+// several lanes hold the minimum (o == kNone with j != kNone means "not loaded").
+// Leaves (d, j) uniform; o is the winner's original index if it was needed, else kNone.
+__device__ __forceinline__ void warp_argmin_redux(double& d, uint32_t& o, uint32_t& j,
+                                                  const uint32_t* __restrict__ orig_of, uint32_t lane) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+    const uint32_t hi = (uint32_t)(bits >> 32), lo = (uint32_t)bits;
+    const uint32_t hmin = __reduce_min_sync(kFull, hi);
+    const uint32_t lmin = __reduce_min_sync(kFull, hi == hmin ? lo : 0xffffffffu);
+    const unsigned holders = __ballot_sync(kFull, j != kNone && hi == hmin && lo == lmin);
+    if (holders == 0) return;  // no candidate anywhere (every d is +inf)
+    int src;
+    if (__popc(holders) == 1) {
+        src = __ffs(holders) - 1;
+        o = kNone;
+    } else {
+        uint32_t mine = 0xffffffffu;
+        if ((holders >> lane) & 1u) mine = (o == kNone) ? ldg_u32(orig_of + j) : o;
+        const uint32_t omin = __reduce_min_sync(kFull, mine);
+        src = __ffs(__ballot_sync(kFull, mine == omin)) - 1;
+        o = omin;
+    }
+    j = __shfl_sync(kFull, j, src);
+    d = __longlong_as_double((long long)(((unsigned long long)hmin << 32) | lmin));
+}
 
 #ifdef PACO_FB_INLINE
 #define PACO_FB_ATTR __forceinline__
 #else
 #define PACO_FB_ATTR __noinline__
 #endif
+
+// Exact nearest unvisited city by (d^2, original index), warp-cooperative.
+// F0: the 32-nearest list is sorted by the same key, so its first unvisited entry
+//     is the answer whenever one exists (one 128-byte row, one ballot).
+// F1: rings of 8x8-cell superblocks (each a contiguous id range) around cur with
+//     squared rectangle lower bounds. Per ring, each lane tests one superblock (its id
+//     range from the compact sb_start table, its free bits from the shared-memory
+//     bitmap); the unvisited ids of every surviving superblock are appended to a shared
+//     list, and the list is scored once, four coordinate loads per lane in flight - one
+//     L2 round trip per ring. A warp argmin closes each ring; its result prunes the
+//     superblocks of the next ring (scoring rings 0 and 1 together, unpruned, measured
+//     slower).
 __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const uint32_t* vis, uint32_t cur,
                                                    uint32_t lane, uint32_t* list, FbStats& fs) {
     {
@@ -321,10 +364,12 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const u
     }
 #ifdef PACO_TIMING
     ++fs.searches;
-    long long tp0 = clock64();
 #endif
     const GridParams& g = a.g;
-    const double2 q = a.xy[cur];
+    const double2* __restrict__ xy = a.xy;
+    const uint32_t* __restrict__ orig_of = a.orig_of;
+    const uint32_t* __restrict__ sb_start = a.sb_start;
+    const double2 q = ldg_d2(xy + cur);
     const int32_t cx = cell_coord(q.x, g.x0, g.inv, g.gw), cy = cell_coord(q.y, g.y0, g.inv, g.gh);
     double bd = __longlong_as_double(0x7ff0000000000000LL);
     uint32_t bo = kNone, bj = kNone;  // bo == kNone with bj != kNone: original index not loaded yet
@@ -333,48 +378,64 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const u
     const int32_t rmax = g.gws > g.ghs ? g.gws : g.ghs;
     const double span = 8.0 * g.cs;
     const unsigned lt_mask = (1u << lane) - 1u;
-    auto score = [&](uint32_t j) {
-        const double d = dist2(q, a.xy[j]);
-        if (d < bd) { bd = d; bj = j; bo = kNone; }
-        else if (d == bd) {
-            if (bo == kNone && bj != kNone) bo = a.orig_of[bj];
-            const uint32_t o = a.orig_of[j];
-            if (o < bo) { bj = j; bo = o; }
+    uint32_t n_list = 0;
+    // score every listed id against the lane's best, four loads in flight per lane
+    auto flush = [&]() {
+        __syncwarp();
+        for (uint32_t t0 = 0; t0 < n_list; t0 += 128) {
+            uint32_t jj[4];
+            double2 pp[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t t = t0 + 32 * u + lane;
+                jj[u] = t < n_list ? list[t] : kNone;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pp[u] = jj[u] != kNone ? ldg_d2(xy + jj[u]) : q;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (jj[u] == kNone) continue;
+                const double d = dist2(q, pp[u]);
+                if (d < bd) { bd = d; bj = jj[u]; bo = kNone; }
+                else if (d == bd) {
+                    if (bo == kNone && bj != kNone) bo = ldg_u32(orig_of + bj);
+                    const uint32_t o = ldg_u32(orig_of + jj[u]);
+                    if (o < bo) { bj = jj[u]; bo = o; }
+                }
+            }
         }
+#ifdef PACO_TIMING
+        if (lane == 0) fs.cities += n_list;
+#endif
+        n_list = 0;
+        __syncwarp();
     };
-    for (int32_t rho = 0; rho <= rmax; ++rho) {
+    for (int32_t rho = 0; rho <= rmax;) {
         if (rho >= 1) {
             const double lb = (rho - 1) * span - slack;
             if (lb > 0 && lb * lb > bd) break;
         }
 #ifdef PACO_TIMING
         ++fs.rings;
-        if (rho == 0) fs.t_pre += clock64() - tp0;
 #endif
-        const double bound = bd;  // warp-uniform (argmin at the end of every ring)
-        const int32_t cnt_ring = rho == 0 ? 1 : 8 * rho;
-        for (int32_t base = 0; base < cnt_ring; base += 32) {
-#ifdef PACO_TIMING
-            long long tt0 = clock64();
-#endif
+        const double bound = bd;  // warp-uniform (argmin at the end of every pass)
+        const int32_t cnt = rho == 0 ? 1 : 8 * rho;
+        for (int32_t base = 0; base < cnt; base += 32) {
             const int32_t c = base + (int32_t)lane;
             bool cand = false;
             uint32_t rs = 0, re = 0;
-            if (c < cnt_ring) {
+            if (c < cnt) {
                 int32_t x = sx, y = sy;
                 if (rho) ring_cell(rho, c, sx, sy, x, y);
                 if (x >= 0 && y >= 0 && x < g.gws && y < g.ghs &&
                     !(rect_lb2(q, g.x0 + x * span, g.y0 + y * span, span, slack) > bound)) {
                     const uint32_t sbm = morton((uint32_t)x, (uint32_t)y);
-                    rs = a.cell_start[sbm << 6];
-                    re = a.cell_start[(sbm + 1) << 6];
+                    rs = ldg_u32(sb_start + sbm);
+                    re = ldg_u32(sb_start + sbm + 1);
                     cand = range_has_unvisited(vis, rs, re);
                 }
             }
             unsigned ball = __ballot_sync(kFull, cand);
-#ifdef PACO_TIMING
-            long long tt1; asm volatile("mov.u64 %0, %%clock64;" : "=l"(tt1) : "r"(ball)); fs.t_test += tt1 - tt0;
-#endif
             while (ball) {
                 const int src = __ffs(ball) - 1;
                 ball &= ball - 1;
@@ -382,9 +443,8 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const u
 #ifdef PACO_TIMING
                 ++fs.sbs;
 #endif
-                // compact the superblock's unvisited ids into the shared list, 128 ids per
-                // pass: lane l tests bit l of four broadcast bitmap words
-                uint32_t n_list = 0;
+                // append the superblock's unvisited ids, 128 ids per step: lane l tests
+                // bit l of four broadcast bitmap words
                 for (uint32_t j0 = s & ~31u; j0 < e; j0 += 128) {
                     uint32_t fb[4];
 #pragma unroll
@@ -397,28 +457,13 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const u
                         if ((fb[q4] >> lane) & 1u) list[n_list + __popc(fb[q4] & lt_mask)] = j0 + 32 * q4 + lane;
                         n_list += __popc(fb[q4]);
                     }
-                    if (n_list > kFbList - 128 || j0 + 128 >= e) {
-                        __syncwarp();
-                        for (uint32_t t = lane; t < n_list; t += 32) score(list[t]);
-#ifdef PACO_TIMING
-                        if (lane == 0) fs.cities += n_list;
-#endif
-                        n_list = 0;
-                        __syncwarp();
-                    }
+                    if (n_list > kFbList - 128) flush();
                 }
             }
-#ifdef PACO_TIMING
-            { long long tt2; asm volatile("mov.u64 %0, %%clock64;" : "=l"(tt2) : "l"(__double_as_longlong(bd))); fs.t_scan += tt2 - tt1; }
-#endif
         }
-#ifdef PACO_TIMING
-        long long ta0 = clock64();
-#endif
-        warp_argmin_lazy(bd, bo, bj, a.orig_of, lane);
-#ifdef PACO_TIMING
-        { long long ta1; asm volatile("mov.u64 %0, %%clock64;" : "=l"(ta1) : "r"(bj)); fs.t_argmin += ta1 - ta0; }
-#endif
+        if (n_list) flush();
+        warp_argmin_redux(bd, bo, bj, orig_of, lane);
+        ++rho;
     }
     return bj;
 }
@@ -450,6 +495,11 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 }
 __device__ __forceinline__ void red_or_shared(uint32_t addr, uint32_t v) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32_if(uint32_t addr, uint32_t v, bool cond) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
+                 "r"((uint32_t)cond)
+                 : "memory");
 }
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
@@ -500,7 +550,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
         return pick_word(v, slot & 3);
     };
     __shared__ FallbackCtx fctx;
-    if (lane == 0) { fctx.knn32 = a.knn32; fctx.xy = a.xy; fctx.orig_of = a.orig_of; fctx.cell_start = a.cell_start; fctx.g = a.g; }
+    if (lane == 0) { fctx.knn32 = a.knn32; fctx.xy = a.xy; fctx.orig_of = a.orig_of; fctx.sb_start = a.sb_start; fctx.g = a.g; }
     for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
     __syncwarp();
     if (lane == 0 && (n & 31)) vis[nw - 1] = 0xffffffffu << (n & 31);  // padding bits count as visited
@@ -546,9 +596,8 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     }
     __syncwarp();
 
-    uint32_t n_dec = 0, n_fb = 0, n_tie = 0, n_forced = 0;
-    uint4 pb = make_uint4(0, 0, 0, 0);  // Philox block of this lane for the current 128-decision batch
-    uint32_t remaining = n - pos;
+    uint32_t n_fb = 0, n_tie = 0;
+    const uint32_t n_dec = n - pos;       // decisions of this construction (the last one forced)
     const uint32_t vis_s = (uint32_t)__cvta_generic_to_shared(vis);
     const uint32_t warm_s = ((vis_s + nw * 4 + 15) & ~15u) + lane * 16;  // L1-warming scratch
     // lanes >= k never load: they hold (cur, 0.0f), and cur is always marked visited
@@ -558,30 +607,29 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     FbStats fs;
 #ifdef PACO_TIMING
     const long long loop0 = clock64();
-    long long seg0 = 0, seg1 = 0, seg2 = 0, segn = 0, fbc = 0;
+    long long fbc = 0;
+    long long pb_t = clock64(), pb_fb = 0, pb_s = 0, pb_r = 0;
+    uint32_t pb_bucket = 0;
 #endif
-    uint32_t uw = 0;  // draw word of the current decision (slot 4 + t)
-    if (!BUF) {
-        pb = philox10(make_uint4(1 + lane, ant, iter_lo, iter_hi), key);
-        uw = __shfl_sync(kFull, pb.x, 0);
-    } else if (remaining > 1) {
-        uw = wrow[4];
-    }
     // candidate row entry of the current decision
-    uint2 e_pre = ldg_u64_if(row_base + (size_t)cur * kp, lane_in && remaining > 1, make_uint2(cur, 0u));
-    for (uint32_t t = 0; remaining > 0; ++t, --remaining) {
-        uint32_t next;
-        ++n_dec;
-        if (remaining > 1) {
+    const uint32_t n_free = n_dec > 0 ? n_dec - 1 : 0;  // roulette / fallback decisions
+    uint2 e_pre = ldg_u64_if(row_base + (size_t)cur * kp, lane_in && n_free > 0, make_uint2(cur, 0u));
+    // Decisions in batches of 128: each lane holds the Philox block of 4 decisions of the
+    // batch (draw slot 4 + t), handed out by shuffle. Inside a batch the only branch is
+    // the (warp-uniform, vote-derived) roulette / fallback split.
+    for (uint32_t t0 = 0; t0 < n_free; t0 += 128) {
+        uint4 pb = make_uint4(0, 0, 0, 0);
+        if (!BUF) pb = philox10(make_uint4(1 + (t0 >> 2) + lane, ant, iter_lo, iter_hi), key);
+        const uint32_t t1 = t0 + 128 < n_free ? t0 + 128 : n_free;
+        for (uint32_t t = t0; t < t1; ++t) {
             __syncwarp();  // orders the previous decision's visited-bit update for every lane
-            PACO_CLOCK(ta, t);
             const uint2 e = e_pre;  // requested at the end of the previous decision
             // feasibility from the bitmap
-            const uint32_t vw = lds_u32(vis_s + ((e.x >> 5) << 2));
-            const float w = ((vw >> (e.x & 31)) & 1u) ? 0.0f : __uint_as_float(e.y);
-            PACO_CLOCK(tb, __float_as_uint(w));
-            // Hillis-Steele inclusive scan over the candidate lanes
-            float v = w;
+            const uint32_t vw_addr = vis_s + ((e.x >> 5) << 2);
+            const uint32_t vw = lds_u32(vw_addr);
+            const uint32_t uw = BUF ? wrow[4 + t] : __shfl_sync(kFull, pick_word(pb, t & 3), (t & 127) >> 2);
+            const uint32_t bit = 1u << (e.x & 31);
+            const float w = (vw & bit) ? 0.0f : __uint_as_float(e.y);
             // Pull every feasible candidate's row into L1 with predicated cp.async.ca (one
             // 16-byte copy per 32-byte sector into a per-lane scratch slot that is never
             // read): the winner's row is then an L1 hit for the next decision.
@@ -596,62 +644,72 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
                     for (uint32_t c = 0; c < (kp * 8 + 31) / 32; ++c) cp_async16_if(warm_s, src + 32 * c, cp);
                 }
             }
+            // S > 0 exactly when some candidate is feasible (a sum of non-negative f32 is at
+            // least its largest term), so the split is decided by a vote the compiler knows
+            // to be warp-uniform
+            const unsigned feas = __ballot_sync(kFull, w > 0.0f);
+            // Hillis-Steele inclusive scan over the candidate lanes
+            float v = w;
 #pragma unroll
             for (int st = 0; st < STEPS; ++st) {
                 const float y = __shfl_up_sync(kFull, v, 1u << st);
                 if (lane >= (1u << st)) v = __fadd_rn(v, y);
             }
-            const float u = u01_f32(uw);
-            const float S = __shfl_sync(kFull, v, k - 1);
-            PACO_CLOCK(tc, __float_as_uint(S));
-            if (S > 0.0f) {
+            uint32_t next;
+            if (feas) {
+                const float u = u01_f32(uw);
+                const float S = __shfl_sync(kFull, v, k - 1);
                 const float target = __fmul_rn(u, S);
                 const float tol = __fmul_rn(1e-6f, S);
                 // only feasible lanes (w > 0; lanes >= k have w = 0) may win: the tree-shaped
                 // scan is not monotone in f32, so an infeasible lane's S_r can exceed its left
-                // neighbour's by an ulp. The three votes are independent and issue together.
+                // neighbour's by an ulp. The two votes are independent and issue together.
                 const unsigned ball = __ballot_sync(kFull, w > 0.0f && v > target);
-                const unsigned feas = __ballot_sync(kFull, w > 0.0f);
                 const unsigned tie = __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(v, target)) <= tol);
                 const int r = ball ? __ffs(ball) - 1 : 31 - __clz(feas);
                 next = __shfl_sync(kFull, e.x, r);
+                // the visit of next: the winning lane already holds next's bitmap word (nothing
+                // has written the bitmap since it was read), so a predicated plain store does
+                // it - no atomic, no branch. No candidate of next is next itself, so the next
+                // decision's probe does not depend on it.
+                sts_u32_if(vw_addr, vw | bit, lane == (uint32_t)r);
                 n_tie += tie ? 1u : 0u;
-                PACO_CLOCK(td, next);
-#ifdef PACO_TIMING
-                seg0 += tb - ta; seg1 += tc - tb; seg2 += td - tc; ++segn;
-#endif
             } else {
 #ifdef PACO_TIMING
                 const long long c0 = clock64();
 #endif
                 next = nearest_unvisited(fctx, vis, cur, lane, fb_list, fs);
+                if (lane == 0) vis[next >> 5] |= 1u << (next & 31);
 #ifdef PACO_TIMING
                 fbc += clock64() - c0;
 #endif
                 ++n_fb;
             }
-        } else {
-            __syncwarp();
-            next = last_unvisited(vis, nw, lane);
-            ++n_forced;
-        }
-        // head of the next decision's dependent chain, issued before any bookkeeping
-        e_pre = ldg_u64_if(row_base + (size_t)next * kp, lane_in, make_uint2(next, 0u));
-        // off-chain bookkeeping overlapping the load: the visit of next (one lane,
-        // fire-and-forget; no candidate of next is next itself), the tour entry and the
-        // next decision's draw word
-        red_or_shared_if(vis_s + ((next >> 5) << 2), 1u << (next & 31), lane == 0);
-        stg_u32_if(out + pos, next, lane == 0);
-        ++pos;
-        cur = next;
-        if (!BUF) {
-            const uint32_t t1 = t + 1;
-            if ((t1 & 127) == 0) pb = philox10(make_uint4(1 + (t1 >> 2) + lane, ant, iter_lo, iter_hi), key);
-            uw = __shfl_sync(kFull, pick_word(pb, t1 & 3), (t1 & 127) >> 2);
-        } else if (remaining > 2) {
-            uw = wrow[4 + t + 1];
+#ifdef PACO_TIMING
+            if (blockIdx.x == 0 && !partial && lane == 0) {
+                const uint32_t bk = (uint32_t)(((uint64_t)pos * 20) / n);
+                if (bk != pb_bucket || t + 1 == n_free) {
+                    const long long now = clock64();
+                    g_prof[pb_bucket] = now - pb_t; g_prof[24 + pb_bucket] = n_fb - pb_fb;
+                    g_prof[48 + pb_bucket] = fs.searches - pb_s; g_prof[72 + pb_bucket] = fs.rings - pb_r;
+                    pb_t = now; pb_fb = n_fb; pb_s = fs.searches; pb_r = fs.rings; pb_bucket = bk;
+                }
+            }
+#endif
+            // head of the next decision's dependent chain, issued before any bookkeeping
+            e_pre = ldg_u64_if(row_base + (size_t)next * kp, lane_in, make_uint2(next, 0u));
+            stg_u32_if(out + pos, next, lane == 0);
+            ++pos;
+            cur = next;
         }
     }
+    if (n_dec > 0) {  // the single remaining city is appended unscored (construction.hpp:529-535)
+        __syncwarp();
+        const uint32_t last = last_unvisited(vis, nw, lane);
+        if (lane == 0) out[pos] = last;
+        ++pos;
+    }
+    const uint32_t n_forced = n_dec > 0 ? 1u : 0u;
     cp_async_wait_all();
     __syncwarp();
 #ifdef PACO_TIMING
@@ -659,8 +717,6 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
         atomicAdd(&g_timing[0], (unsigned long long)(clock64() - loop0));
         atomicAdd(&g_timing[1], (unsigned long long)fbc);
         atomicAdd(&g_timing[2], (unsigned long long)n_dec);
-        atomicAdd(&g_timing[4], (unsigned long long)seg0); atomicAdd(&g_timing[5], (unsigned long long)seg1);
-        atomicAdd(&g_timing[6], (unsigned long long)seg2); atomicAdd(&g_timing[7], (unsigned long long)segn);
     }
     {
         long long c = fs.cities;
@@ -668,8 +724,6 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
         if (lane == 0) {
             atomicAdd(&g_timing[9], (unsigned long long)fs.searches); atomicAdd(&g_timing[10], (unsigned long long)fs.rings);
             atomicAdd(&g_timing[11], (unsigned long long)fs.sbs); atomicAdd(&g_timing[12], (unsigned long long)c);
-            atomicAdd(&g_timing[13], (unsigned long long)fs.t_test); atomicAdd(&g_timing[14], (unsigned long long)fs.t_scan);
-            atomicAdd(&g_timing[15], (unsigned long long)fs.t_argmin); atomicAdd(&g_timing[3], (unsigned long long)fs.t_pre);
         }
     }
 #endif

@@ -59,7 +59,7 @@ struct paco_handle {
     std::vector<uint32_t> h_orig, h_int;
     // device
     double2* xy = nullptr;
-    uint32_t *orig_of = nullptr, *int_of = nullptr, *cell_start = nullptr;
+    uint32_t *orig_of = nullptr, *int_of = nullptr, *cell_start = nullptr, *sb_start = nullptr;
     uint32_t* knn = nullptr;
     float* eta = nullptr;
     uint2* cand = nullptr;
@@ -89,7 +89,7 @@ struct paco_handle {
 
     ~paco_handle() {
         if (dev >= 0) cudaSetDevice(dev);
-        void* ptrs[] = {xy, orig_of, int_of, cell_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
+        void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
                         partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, counters, err, words,
                         scratch_u32, scratch_u64, rng, ratio, Tfull};
         for (void* p : ptrs)
@@ -266,6 +266,7 @@ static paco_status setup(paco_handle* h) {
     CU(dalloc(&dx, n)); CU(dalloc(&dy, n));
     CU(dalloc(&keys, n)); CU(dalloc(&keys2, n)); CU(dalloc(&cellm, n));
     CU(dalloc(&h->cell_start, (size_t)h->g.ncells + 1));
+    CU(dalloc(&h->sb_start, (size_t)(h->g.ncells >> 6) + 1));
     CU(dalloc(&h->knn, (size_t)n * 32)); CU(dalloc(&h->eta, (size_t)n * k)); CU(dalloc(&h->cand, (size_t)n * h->kp));
     CU(cudaMemsetAsync(h->cand, 0, sizeof(uint2) * (size_t)n * h->kp, st));
     if (h->mode == PACO_MODE_CLASSIC) {
@@ -291,6 +292,10 @@ static paco_status setup(paco_handle* h) {
     CU(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, keys2, (int)n, 0, end_bit, st));
     k_scatter<<<nb, tb, 0, st>>>(keys2, dx, dy, n, h->xy, h->orig_of, h->int_of, cellm);
     k_cell_start<<<nb, tb, 0, st>>>(cellm, n, h->g.ncells, h->cell_start);
+    {
+        const uint32_t nsb = h->g.ncells >> 6;
+        k_sb_start<<<(nsb + 1 + 255) / 256, 256, 0, st>>>(h->cell_start, nsb, h->sb_start);
+    }
     CU(cudaGetLastError());
     // K1: k-NN over superblocks, staged in shared memory (cap cities per CTA)
     const uint32_t cap = 6144;
@@ -425,7 +430,7 @@ static paco_status launch_construct_ir(paco_handle* h, bool seeding) {
 static ConstructArgs construct_args(paco_handle* h, bool seeding) {
     ConstructArgs a{};
     a.cand = h->cand; a.knn32 = h->knn; a.xy = h->xy; a.orig_of = h->orig_of; a.int_of = h->int_of;
-    a.cell_start = h->cell_start; a.g = h->g; a.tours = h->tours; a.lb_sel = h->lb_sel;
+    a.sb_start = h->sb_start; a.g = h->g; a.tours = h->tours; a.lb_sel = h->lb_sel;
     a.new_len = h->new_len; a.partial_flag = h->partial; a.counters = h->counters;
     a.words = h->cfg.draws == PACO_DRAWS_BUFFER ? h->words : nullptr;
     a.stride = h->words_stride; a.seed = h->cfg.seed; a.iter = h->iter;
@@ -650,6 +655,7 @@ paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, u
 }
 
 #ifdef PACO_TIMING
+extern "C" void paco_debug_prof(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 96); }
 extern "C" void paco_debug_timing(unsigned long long* out, int reset) {
     cudaMemcpyFromSymbol(out, g_timing, sizeof(unsigned long long) * 16);
     if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_timing, z, sizeof z); }
