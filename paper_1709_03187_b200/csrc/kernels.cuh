@@ -598,8 +598,11 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
 
     uint32_t n_fb = 0, n_tie = 0;
     const uint32_t n_dec = n - pos;       // decisions of this construction (the last one forced)
-    const uint32_t vis_s = (uint32_t)__cvta_generic_to_shared(vis);
-    const uint32_t warm_s = ((vis_s + nw * 4 + 15) & ~15u) + lane * 16;  // L1-warming scratch
+    // shared-window addresses pinned in registers (an opaque move keeps the compiler from
+    // re-deriving them from SR_CgaCtaId inside the loop, on the probe's address path)
+    uint32_t vis_s, warm_s;
+    asm volatile("mov.b32 %0, %1;" : "=r"(vis_s) : "r"((uint32_t)__cvta_generic_to_shared(vis)));
+    asm volatile("mov.b32 %0, %1;" : "=r"(warm_s) : "r"(((vis_s + nw * 4 + 15) & ~15u) + lane * 16));  // L1-warming scratch
     // lanes >= k never load: they hold (cur, 0.0f), and cur is always marked visited
     const bool lane_in = lane < k;
     const uint2* __restrict__ row_base = a.cand + lane;
@@ -664,15 +667,19 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
                 // only feasible lanes (w > 0; lanes >= k have w = 0) may win: the tree-shaped
                 // scan is not monotone in f32, so an infeasible lane's S_r can exceed its left
                 // neighbour's by an ulp. The two votes are independent and issue together.
-                const unsigned ball = __ballot_sync(kFull, w > 0.0f && v > target);
+                // The pick as two integer min-reductions over (lane, city) keys - lowest winning
+                // lane, else highest feasible lane - which deliver the city itself (city ids are
+                // < 2^21 since the bitmap fits in shared memory), with no ffs and no shuffle.
+                const uint32_t kw = __reduce_min_sync(kFull, (w > 0.0f && v > target) ? ((lane << 27) | e.x) : kNone);
+                const uint32_t kf = __reduce_min_sync(kFull, w > 0.0f ? (((31u - lane) << 27) | e.x) : kNone);
                 const unsigned tie = __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(v, target)) <= tol);
-                const int r = ball ? __ffs(ball) - 1 : 31 - __clz(feas);
-                next = __shfl_sync(kFull, e.x, r);
+                const uint32_t r = kw != kNone ? (kw >> 27) : 31u - (kf >> 27);
+                next = (kw != kNone ? kw : kf) & 0x07ffffffu;
                 // the visit of next: the winning lane already holds next's bitmap word (nothing
                 // has written the bitmap since it was read), so a predicated plain store does
                 // it - no atomic, no branch. No candidate of next is next itself, so the next
                 // decision's probe does not depend on it.
-                sts_u32_if(vw_addr, vw | bit, lane == (uint32_t)r);
+                sts_u32_if(vw_addr, vw | bit, lane == r);
                 n_tie += tie ? 1u : 0u;
             } else {
 #ifdef PACO_TIMING
