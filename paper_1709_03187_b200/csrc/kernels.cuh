@@ -292,6 +292,35 @@ struct FbStats {
 #endif
 };
 
+__device__ __forceinline__ uint2 lds_u64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void red_or_shared(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32_if(uint32_t addr, uint32_t v, bool cond) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
+                 "r"((uint32_t)cond)
+                 : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+// predicated 16-byte global->shared async copy (LDGSTS), L1-allocating
+__device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, bool cond) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 16;\n\t}" ::"r"(dst),
+                 "l"(src), "r"((uint32_t)cond));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 constexpr uint32_t kFbList = 256;  // per-warp shared-memory list of unvisited city ids (fallback)
 
 // Everything the fallback reads, kept in shared memory so the (rarely executed)
@@ -355,11 +384,44 @@ __device__ __forceinline__ void warp_argmin_redux(double& d, uint32_t& o, uint32
 //     L2 round trip per ring. A warp argmin closes each ring; its result prunes the
 //     superblocks of the next ring (scoring rings 0 and 1 together, unpruned, measured
 //     slower).
-__device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const uint32_t* vis, uint32_t cur,
-                                                   uint32_t lane, uint32_t* list, FbStats& fs) {
+__device__ __forceinline__ uint32_t lds_u32_if(uint32_t addr, bool cond, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}" : "+r"(v) : "r"(addr), "r"((uint32_t)cond));
+    return v;
+}
+// any unvisited city in the internal id range [s, e)? (bitmap at shared address vis_s;
+// the words are read four at a time, independently)
+__device__ __forceinline__ bool range_has_unvisited_s(uint32_t vis_s, uint32_t s, uint32_t e) {
+    if (s >= e) return false;
+    const uint32_t w0 = s >> 5, w1 = (e - 1) >> 5;
+    const uint32_t m0 = 0xffffffffu << (s & 31), m1 = 0xffffffffu >> (31 - ((e - 1) & 31));
+    uint32_t any = 0;
+    for (uint32_t w = w0; w <= w1; w += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t ww = w + q;
+            uint32_t f = ~lds_u32_if(vis_s + 4 * ww, ww <= w1, ~0u);
+            if (ww == w0) f &= m0;
+            if (ww == w1) f &= m1;
+            any |= f;
+        }
+    }
+    return any != 0;
+}
+// unvisited bits of bitmap word w restricted to the id range [s, e) (0 unless cond)
+__device__ __forceinline__ uint32_t free_bits_s(uint32_t vis_s, uint32_t w, uint32_t s, uint32_t e, bool cond) {
+    uint32_t fb = ~lds_u32_if(vis_s + 4 * w, cond, ~0u);
+    if (w == (s >> 5)) fb &= 0xffffffffu << (s & 31);
+    if (w == ((e - 1) >> 5)) fb &= 0xffffffffu >> (31 - ((e - 1) & 31));
+    return fb;
+}
+
+__device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_t vis_s, uint32_t cur,
+                                                   uint32_t lane, uint32_t list_s, FbStats& fs) {
     {
         const uint32_t c = ldg_u32(&a.knn32[(size_t)cur * 32 + lane]);
-        const unsigned b = __ballot_sync(kFull, c != kNone && !is_visited(vis, c));
+        const bool ok = c != kNone;
+        const uint32_t vw = lds_u32_if(vis_s + ((c >> 5) << 2), ok, ~0u);
+        const unsigned b = __ballot_sync(kFull, ok && !((vw >> (c & 31)) & 1u));
         if (b) return __shfl_sync(kFull, c, __ffs(b) - 1);
     }
 #ifdef PACO_TIMING
@@ -388,7 +450,7 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const u
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t t = t0 + 32 * u + lane;
-                jj[u] = t < n_list ? list[t] : kNone;
+                jj[u] = lds_u32_if(list_s + 4 * t, t < n_list, kNone);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) pp[u] = jj[u] != kNone ? ldg_d2(xy + jj[u]) : q;
@@ -421,6 +483,9 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const u
         const double bound = bd;  // warp-uniform (argmin at the end of every pass)
         const int32_t cnt = rho == 0 ? 1 : 8 * rho;
         for (int32_t base = 0; base < cnt; base += 32) {
+#ifdef PACO_TIMING
+            long long tt0 = clock64();
+#endif
             const int32_t c = base + (int32_t)lane;
             bool cand = false;
             uint32_t rs = 0, re = 0;
@@ -432,10 +497,13 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const u
                     const uint32_t sbm = morton((uint32_t)x, (uint32_t)y);
                     rs = ldg_u32(sb_start + sbm);
                     re = ldg_u32(sb_start + sbm + 1);
-                    cand = range_has_unvisited(vis, rs, re);
+                    cand = range_has_unvisited_s(vis_s, rs, re);
                 }
             }
             unsigned ball = __ballot_sync(kFull, cand);
+#ifdef PACO_TIMING
+            { long long tt1; asm volatile("mov.u64 %0, %%clock64;" : "=l"(tt1) : "r"(ball)); fs.t_test += tt1 - tt0; tt0 = tt1; }
+#endif
             while (ball) {
                 const int src = __ffs(ball) - 1;
                 ball &= ball - 1;
@@ -450,19 +518,31 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, const u
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
                         const uint32_t w = (j0 >> 5) + q4;
-                        fb[q4] = (j0 + 32 * q4 < e) ? free_bits(vis, w, s, e) : 0u;
+                        fb[q4] = free_bits_s(vis_s, w, s, e, j0 + 32 * q4 < e);
                     }
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
-                        if ((fb[q4] >> lane) & 1u) list[n_list + __popc(fb[q4] & lt_mask)] = j0 + 32 * q4 + lane;
+                        sts_u32_if(list_s + 4 * (n_list + __popc(fb[q4] & lt_mask)), j0 + 32 * q4 + lane, (fb[q4] >> lane) & 1u);
                         n_list += __popc(fb[q4]);
                     }
                     if (n_list > kFbList - 128) flush();
                 }
             }
+#ifdef PACO_TIMING
+            { long long tt2; asm volatile("mov.u64 %0, %%clock64;" : "=l"(tt2) : "r"(n_list)); fs.t_pre += tt2 - tt0; }
+#endif
         }
+#ifdef PACO_TIMING
+        long long ts0 = clock64();
+#endif
         if (n_list) flush();
+#ifdef PACO_TIMING
+        long long ts1; asm volatile("mov.u64 %0, %%clock64;" : "=l"(ts1) : "l"(__double_as_longlong(bd))); fs.t_scan += ts1 - ts0;
+#endif
         warp_argmin_redux(bd, bo, bj, orig_of, lane);
+#ifdef PACO_TIMING
+        { long long ts2; asm volatile("mov.u64 %0, %%clock64;" : "=l"(ts2) : "r"(bj)); fs.t_argmin += ts2 - ts1; }
+#endif
         ++rho;
     }
     return bj;
@@ -482,35 +562,6 @@ __device__ __forceinline__ uint32_t last_unvisited(const uint32_t* vis, uint32_t
     }
     return kNone;
 }
-
-__device__ __forceinline__ uint2 lds_u64(uint32_t addr) {
-    uint2 v;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ void red_or_shared(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void sts_u32_if(uint32_t addr, uint32_t v, bool cond) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
-                 "r"((uint32_t)cond)
-                 : "memory");
-}
-__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
-}
-// predicated 16-byte global->shared async copy (LDGSTS), L1-allocating
-__device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, bool cond) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 16;\n\t}" ::"r"(dst),
-                 "l"(src), "r"((uint32_t)cond));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 #ifdef PACO_TIMING
 #define PACO_CLOCK(var, dep) long long var; asm volatile("mov.u64 %0, %%clock64;" : "=l"(var) : "r"(dep))
@@ -600,8 +651,9 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     const uint32_t n_dec = n - pos;       // decisions of this construction (the last one forced)
     // shared-window addresses pinned in registers (an opaque move keeps the compiler from
     // re-deriving them from SR_CgaCtaId inside the loop, on the probe's address path)
-    uint32_t vis_s, warm_s;
+    uint32_t vis_s, warm_s, fb_s;
     asm volatile("mov.b32 %0, %1;" : "=r"(vis_s) : "r"((uint32_t)__cvta_generic_to_shared(vis)));
+    asm volatile("mov.b32 %0, %1;" : "=r"(fb_s) : "r"((uint32_t)__cvta_generic_to_shared(fb_list)));
     asm volatile("mov.b32 %0, %1;" : "=r"(warm_s) : "r"(((vis_s + nw * 4 + 15) & ~15u) + lane * 16));  // L1-warming scratch
     // lanes >= k never load: they hold (cur, 0.0f), and cur is always marked visited
     const bool lane_in = lane < k;
@@ -685,7 +737,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
 #ifdef PACO_TIMING
                 const long long c0 = clock64();
 #endif
-                next = nearest_unvisited(fctx, vis, cur, lane, fb_list, fs);
+                next = nearest_unvisited(fctx, vis_s, cur, lane, fb_s, fs);
                 if (lane == 0) vis[next >> 5] |= 1u << (next & 31);
 #ifdef PACO_TIMING
                 fbc += clock64() - c0;
@@ -731,6 +783,8 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
         if (lane == 0) {
             atomicAdd(&g_timing[9], (unsigned long long)fs.searches); atomicAdd(&g_timing[10], (unsigned long long)fs.rings);
             atomicAdd(&g_timing[11], (unsigned long long)fs.sbs); atomicAdd(&g_timing[12], (unsigned long long)c);
+            atomicAdd(&g_timing[13], (unsigned long long)fs.t_test); atomicAdd(&g_timing[14], (unsigned long long)fs.t_scan);
+            atomicAdd(&g_timing[15], (unsigned long long)fs.t_argmin); atomicAdd(&g_timing[3], (unsigned long long)fs.t_pre);
         }
     }
 #endif
