@@ -54,12 +54,8 @@ __global__ void k_sb_start(const uint32_t* __restrict__ cell_start, uint32_t nsb
 }
 
 // ============================================================ K1: k-NN lists
-// Per city: the k nearest other cities by (d^2, original index). One CTA per
-// superblock; the 3x3 superblock neighbourhood is staged in shared memory when it
-// fits, and a city whose k-th key is not certified by the staged region's border
-// (sparse areas, dense clusters) falls back to an exact ring search over global
-// memory. Output rows are in internal ids; eta^beta (construction.hpp:46-61) is
-// emitted alongside.
+// Per city: the k nearest other cities by (d^2, original index), rows in internal
+// ids; eta^beta (construction.hpp:46-61) is emitted alongside.
 template <int KMAX>
 struct TopK {
     double d[KMAX];
@@ -78,6 +74,11 @@ struct TopK {
             }
         }
         if (key_less(dd, oo, d[0], o[0])) { d[0] = dd; o[0] = oo; j[0] = jj; }
+    }
+    // the original index (tie-break key) is read only for a candidate that can enter
+    __device__ __forceinline__ void offer_lazy(double dd, uint32_t jj, const uint32_t* __restrict__ orig_of, int k) {
+        if (dd > d[k - 1]) return;
+        offer(dd, orig_of[jj], jj, k);
     }
 };
 
@@ -104,7 +105,7 @@ __device__ void knn_ring_search(uint32_t i, double2 q, const double2* __restrict
             for (uint32_t jj = s; jj < e; ++jj) {
                 if (jj == i) continue;
                 ++found;
-                t.offer(dist2(q, xy[jj]), orig_of[jj], jj, k);
+                t.offer_lazy(dist2(q, xy[jj]), jj, orig_of, k);
             }
         }
     }
@@ -125,77 +126,23 @@ __device__ void knn_emit(uint32_t i, double2 q, const TopK<KMAX>& t, int kk, int
     }
 }
 
+// One thread per city (internal id order, so a CTA covers a compact patch and its cell
+// scans share L1 lines), exact ring search over grid cells until the ring's lower bound
+// exceeds the current k-th key. Work per city follows the local density (about 100
+// candidates in uniform areas). A superblock-staged variant (3x3 superblocks in shared
+// memory, one CTA per superblock) measured 14x slower at C5: in dense clusters every
+// city scanned thousands of staged cities, and the 147 KB stage allowed one CTA per SM.
 template <int KMAX>
-__global__ void __launch_bounds__(128) k_knn(const double2* __restrict__ xy, const uint32_t* __restrict__ orig_of,
-                                             const uint32_t* __restrict__ cell_start, GridParams g, uint32_t n,
-                                             int kk, int k, double beta, uint32_t cap, uint32_t* __restrict__ knn32,
-                                             float* __restrict__ eta, uint32_t* __restrict__ n_global) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t sb = blockIdx.x;
-    const uint32_t s0 = cell_start[sb << 6], e0 = cell_start[(sb + 1) << 6];
-    if (s0 >= e0) return;
-    const int32_t sbx = (int32_t)compact16(sb), sby = (int32_t)compact16(sb >> 1);
-    // staged neighbourhood: up to 9 contiguous id ranges
-    __shared__ uint32_t rs[9], re[9], roff[10];
-    if (threadIdx.x == 0) {
-        uint32_t off = 0;
-        for (int q = 0; q < 9; ++q) {
-            const int32_t x = sbx + q % 3 - 1, y = sby + q / 3 - 1;
-            uint32_t a = 0, b = 0;
-            if (x >= 0 && y >= 0 && x < g.gws && y < g.ghs) {
-                const uint32_t m = morton((uint32_t)x, (uint32_t)y);
-                a = cell_start[m << 6]; b = cell_start[(m + 1) << 6];
-            }
-            rs[q] = a; re[q] = b; roff[q] = off; off += b - a;
-        }
-        roff[9] = off;
-    }
-    __syncthreads();
-    const uint32_t C = roff[9];
-    const bool staged = C <= cap;
-    double2* sxy = reinterpret_cast<double2*>(smem);
-    uint32_t* so = reinterpret_cast<uint32_t*>(sxy + (staged ? C : 0));
-    uint32_t* sj = so + (staged ? C : 0);
-    if (staged) {
-        for (int q = 0; q < 9; ++q)
-            for (uint32_t p = rs[q] + threadIdx.x; p < re[q]; p += blockDim.x) {
-                const uint32_t dst = roff[q] + (p - rs[q]);
-                sxy[dst] = xy[p]; so[dst] = orig_of[p]; sj[dst] = p;
-            }
-    }
-    __syncthreads();
-    // staged region border (infinite where the region reaches the grid edge)
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
-    const double span = 8.0 * g.cs;
-    const double xlo = sbx >= 2 ? g.x0 + (sbx - 1) * span : -inf;
-    const double xhi = sbx + 2 < g.gws ? g.x0 + (sbx + 2) * span : inf;
-    const double ylo = sby >= 2 ? g.y0 + (sby - 1) * span : -inf;
-    const double yhi = sby + 2 < g.ghs ? g.y0 + (sby + 2) * span : inf;
-    for (uint32_t i = s0 + threadIdx.x; i < e0; i += blockDim.x) {
-        const double2 q = xy[i];
-        TopK<KMAX> t;
-        bool ok = false;
-        if (staged) {
-            t.init();
-            for (uint32_t p = 0; p < C; ++p) {
-                if (sj[p] == i) continue;
-                t.offer(dist2(q, sxy[p]), so[p], sj[p], kk);
-            }
-            double lb = fmin(fmin(q.x - xlo, xhi - q.x), fmin(q.y - ylo, yhi - q.y));
-            if (C >= (uint32_t)kk + 1) {
-                if (lb == inf) ok = true;  // the staged region is the whole instance
-                else {
-                    lb -= 1e-6 * g.cs;
-                    ok = lb > 0 && lb * lb > t.d[kk - 1];
-                }
-            }
-        }
-        if (!ok) {
-            atomicAdd(n_global, 1u);
-            knn_ring_search<KMAX>(i, q, xy, orig_of, cell_start, g, kk, t);
-        }
-        knn_emit<KMAX>(i, q, t, kk, k, xy, beta, knn32, eta);
-    }
+__global__ void __launch_bounds__(128) k_knn_cells(const double2* __restrict__ xy, const uint32_t* __restrict__ orig_of,
+                                                   const uint32_t* __restrict__ cell_start, GridParams g, uint32_t n,
+                                                   int kk, int k, double beta, uint32_t* __restrict__ knn32,
+                                                   float* __restrict__ eta) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double2 q = xy[i];
+    TopK<KMAX> t;
+    knn_ring_search<KMAX>(i, q, xy, orig_of, cell_start, g, kk, t);
+    knn_emit<KMAX>(i, q, t, kk, k, xy, beta, knn32, eta);
 }
 
 // ============================================================ K5: weight table
@@ -417,6 +364,7 @@ __device__ __forceinline__ uint32_t free_bits_s(uint32_t vis_s, uint32_t w, uint
 
 __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_t vis_s, uint32_t cur,
                                                    uint32_t lane, uint32_t list_s, FbStats& fs) {
+    const double2 q = ldg_d2(a.xy + cur);  // issued with the F0 row: F1 needs it first
     {
         const uint32_t c = ldg_u32(&a.knn32[(size_t)cur * 32 + lane]);
         const bool ok = c != kNone;
@@ -431,7 +379,6 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_
     const double2* __restrict__ xy = a.xy;
     const uint32_t* __restrict__ orig_of = a.orig_of;
     const uint32_t* __restrict__ sb_start = a.sb_start;
-    const double2 q = ldg_d2(xy + cur);
     const int32_t cx = cell_coord(q.x, g.x0, g.inv, g.gw), cy = cell_coord(q.y, g.y0, g.inv, g.gh);
     double bd = __longlong_as_double(0x7ff0000000000000LL);
     uint32_t bo = kNone, bj = kNone;  // bo == kNone with bj != kNone: original index not loaded yet
@@ -493,7 +440,7 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_
                 int32_t x = sx, y = sy;
                 if (rho) ring_cell(rho, c, sx, sy, x, y);
                 if (x >= 0 && y >= 0 && x < g.gws && y < g.ghs &&
-                    !(rect_lb2(q, g.x0 + x * span, g.y0 + y * span, span, slack) > bound)) {
+                    (rho == 0 || !(rect_lb2(q, g.x0 + x * span, g.y0 + y * span, span, slack) > bound))) {
                     const uint32_t sbm = morton((uint32_t)x, (uint32_t)y);
                     rs = ldg_u32(sb_start + sbm);
                     re = ldg_u32(sb_start + sbm + 1);
@@ -689,6 +636,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
             // 16-byte copy per 32-byte sector into a per-lane scratch slot that is never
             // read): the winner's row is then an L1 hit for the next decision.
             // prefetch.global.L1 has no measurable effect on B200 (profiles/README.md).
+#ifndef PACO_NO_WARM
             {
                 const bool cp = w > 0.0f;
                 const unsigned char* src = reinterpret_cast<const unsigned char*>(a.cand + (size_t)e.x * kp);
@@ -699,6 +647,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
                     for (uint32_t c = 0; c < (kp * 8 + 31) / 32; ++c) cp_async16_if(warm_s, src + 32 * c, cp);
                 }
             }
+#endif
             // S > 0 exactly when some candidate is feasible (a sum of non-negative f32 is at
             // least its largest term), so the split is decided by a vote the compiler knows
             // to be warp-uniform

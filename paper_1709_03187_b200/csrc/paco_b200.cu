@@ -80,7 +80,6 @@ struct paco_handle {
     uint64_t iter = 0;
     double construct_ms = 0, update_ms = 0, setup_ms = 0;
     std::vector<cudaEvent_t> evpool;
-    uint32_t knn_global_fallbacks = 0;
     // reference-rule (IR) mode
     bool ir = false;
     uint64_t* rng = nullptr;   // m*4 xoshiro256++ states
@@ -297,23 +296,16 @@ static paco_status setup(paco_handle* h) {
         k_sb_start<<<(nsb + 1 + 255) / 256, 256, 0, st>>>(h->cell_start, nsb, h->sb_start);
     }
     CU(cudaGetLastError());
-    // K1: k-NN over superblocks, staged in shared memory (cap cities per CTA)
-    const uint32_t cap = 6144;
-    const size_t smem = (size_t)cap * (sizeof(double2) + 2 * sizeof(uint32_t));
-    const uint32_t nsb = h->g.ncells >> 6;
-    uint32_t* nglob = h->scratch_u32;
-    CU(cudaMemsetAsync(nglob, 0, sizeof(uint32_t), st));
+    // K1: k-NN lists, one thread per city, exact ring search over grid cells
     const int kk = (int)std::min<uint32_t>(32, n - 1);
-    CU(cudaFuncSetAttribute(k_knn<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_knn<32><<<nsb, 128, smem, st>>>(h->xy, h->orig_of, h->cell_start, h->g, n, kk, (int)k, h->cfg.beta, cap,
-                                      h->knn, h->eta, nglob);
+    k_knn_cells<32><<<(n + 127) / 128, 128, 0, st>>>(h->xy, h->orig_of, h->cell_start, h->g, n, kk, (int)k,
+                                                     h->cfg.beta, h->knn, h->eta);
     CU(cudaGetLastError());
     CU(cudaEventRecord(e1, st));
     CU(cudaStreamSynchronize(st));
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, e0, e1));
     h->setup_ms = ms;
-    CU(cudaMemcpy(&h->knn_global_fallbacks, nglob, sizeof(uint32_t), cudaMemcpyDeviceToHost));
     cudaEventDestroy(e0); cudaEventDestroy(e1);
     h->h_orig.resize(n); h->h_int.resize(n);
     CU(cudaMemcpy(h->h_orig.data(), h->orig_of, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
