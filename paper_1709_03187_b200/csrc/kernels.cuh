@@ -652,25 +652,27 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
             // least its largest term), so the split is decided by a vote the compiler knows
             // to be warp-uniform
             const unsigned feas = __ballot_sync(kFull, w > 0.0f);
-            // Hillis-Steele inclusive scan over the candidate lanes
+            // Hillis-Steele inclusive scan over the candidate lanes; S = S_{k-1}. (Forming S
+            // from the two last-level terms by broadcast, or packing the pick into one
+            // reduction, measured slower: the chain is sensitive to how the MIO operations
+            // interleave, profiles/README.md.)
             float v = w;
 #pragma unroll
             for (int st = 0; st < STEPS; ++st) {
                 const float y = __shfl_up_sync(kFull, v, 1u << st);
                 if (lane >= (1u << st)) v = __fadd_rn(v, y);
             }
+            const float S = __shfl_sync(kFull, v, k - 1);
             uint32_t next;
             if (feas) {
                 const float u = u01_f32(uw);
-                const float S = __shfl_sync(kFull, v, k - 1);
                 const float target = __fmul_rn(u, S);
                 const float tol = __fmul_rn(1e-6f, S);
-                // only feasible lanes (w > 0; lanes >= k have w = 0) may win: the tree-shaped
+                // Only feasible lanes (w > 0; lanes >= k have w = 0) may win: the tree-shaped
                 // scan is not monotone in f32, so an infeasible lane's S_r can exceed its left
-                // neighbour's by an ulp. The two votes are independent and issue together.
-                // The pick as two integer min-reductions over (lane, city) keys - lowest winning
-                // lane, else highest feasible lane - which deliver the city itself (city ids are
-                // < 2^21 since the bitmap fits in shared memory), with no ffs and no shuffle.
+                // neighbour's by an ulp. The pick is two integer min-reductions over (lane, city)
+                // keys - lowest winning lane, else highest feasible lane - which deliver the
+                // city itself (ids < 2^21: the bitmap fits in shared memory), no ffs, no shuffle.
                 const uint32_t kw = __reduce_min_sync(kFull, (w > 0.0f && v > target) ? ((lane << 27) | e.x) : kNone);
                 const uint32_t kf = __reduce_min_sync(kFull, w > 0.0f ? (((31u - lane) << 27) | e.x) : kNone);
                 const unsigned tie = __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(v, target)) <= tol);

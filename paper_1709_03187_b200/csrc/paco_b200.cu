@@ -337,6 +337,8 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
     (void)kpp;
     const bool ir = cfg->rule == PACO_RULE_INDEPENDENT_ROULETTE;
     const size_t smem_need = ir ? ir_smem_bytes(n, nwords, mode) : kFbList * 4 + (size_t)nwords * 4;
+    if (!ir && n >= (1u << 21))  // the pick packs city ids into 21 bits (implied by the bitmap bound below)
+        return fail(PACO_E_UNSUPPORTED, "visited bitmap exceeds shared memory (n too large)");
     if (smem_need > (size_t)prop.sharedMemPerBlockOptin)
         return fail(PACO_E_UNSUPPORTED, ir ? "reference-rule per-ant state exceeds shared memory (n too large)"
                                            : "visited bitmap exceeds shared memory (n too large)");
