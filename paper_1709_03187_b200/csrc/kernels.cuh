@@ -56,44 +56,68 @@ __global__ void k_sb_start(const uint32_t* __restrict__ cell_start, uint32_t nsb
 // ============================================================ K1: k-NN lists
 // Per city: the k nearest other cities by (d^2, original index), rows in internal
 // ids; eta^beta (construction.hpp:46-61) is emitted alongside.
+// Bounded max-heap of the KMAX smallest (d^2, original index) keys seen so far (root =
+// current worst), for the long near lists: an accepted candidate costs O(log KMAX)
+// instead of the O(KMAX) shifts of a sorted register list, which for KMAX >= 64 also
+// spills. sort() leaves the keys ascending.
 template <int KMAX>
-struct TopK {
+struct NearHeap {
     double d[KMAX];
     uint32_t o[KMAX], j[KMAX];
-    __device__ void init() {
-#pragma unroll
-        for (int r = 0; r < KMAX; ++r) { d[r] = __longlong_as_double(0x7ff0000000000000LL); o[r] = kNone; j[r] = kNone; }
+    int size;
+    __device__ void init() { size = 0; }
+    __device__ __forceinline__ bool worse(int a, int b) const {  // key[a] > key[b]
+        return key_less(d[b], o[b], d[a], o[a]);
     }
-    __device__ __forceinline__ void offer(double dd, uint32_t oo, uint32_t jj, int k) {
-        if (!key_less(dd, oo, d[k - 1], o[k - 1])) return;
-#pragma unroll
-        for (int r = KMAX - 1; r > 0; --r) {
-            if (r < k) {
-                if (key_less(dd, oo, d[r - 1], o[r - 1])) { d[r] = d[r - 1]; o[r] = o[r - 1]; j[r] = j[r - 1]; }
-                else if (key_less(dd, oo, d[r], o[r])) { d[r] = dd; o[r] = oo; j[r] = jj; }
-            }
+    __device__ __forceinline__ void swap_(int a, int b) {
+        const double td = d[a]; d[a] = d[b]; d[b] = td;
+        const uint32_t to = o[a]; o[a] = o[b]; o[b] = to;
+        const uint32_t tj = j[a]; j[a] = j[b]; j[b] = tj;
+    }
+    __device__ void sift_down(int p, int m) {
+        for (;;) {
+            const int l = 2 * p + 1, r = l + 1;
+            int big = p;
+            if (l < m && worse(l, big)) big = l;
+            if (r < m && worse(r, big)) big = r;
+            if (big == p) return;
+            swap_(p, big);
+            p = big;
         }
-        if (key_less(dd, oo, d[0], o[0])) { d[0] = dd; o[0] = oo; j[0] = jj; }
     }
-    // the original index (tie-break key) is read only for a candidate that can enter
-    __device__ __forceinline__ void offer_lazy(double dd, uint32_t jj, const uint32_t* __restrict__ orig_of, int k) {
-        if (dd > d[k - 1]) return;
-        offer(dd, orig_of[jj], jj, k);
+    __device__ void offer(double dd, uint32_t jj, const uint32_t* __restrict__ orig_of, int k) {
+        if (size == k && dd > d[0]) return;  // cannot enter: the original index is not read
+        const uint32_t oo = orig_of[jj];
+        if (size < k) {
+            int p = size++;
+            d[p] = dd; o[p] = oo; j[p] = jj;
+            while (p > 0) {
+                const int q = (p - 1) / 2;
+                if (!worse(p, q)) break;
+                swap_(p, q);
+                p = q;
+            }
+        } else if (key_less(dd, oo, d[0], o[0])) {
+            d[0] = dd; o[0] = oo; j[0] = jj;
+            sift_down(0, size);
+        }
+    }
+    __device__ void sort() {
+        for (int m = size - 1; m > 0; --m) { swap_(0, m); sift_down(0, m); }
     }
 };
 
 template <int KMAX>
-__device__ void knn_ring_search(uint32_t i, double2 q, const double2* __restrict__ xy,
-                                const uint32_t* __restrict__ orig_of, const uint32_t* __restrict__ cell_start,
-                                const GridParams& g, int k, TopK<KMAX>& t) {
+__device__ void near_ring_search(uint32_t i, double2 q, const double2* __restrict__ xy,
+                                 const uint32_t* __restrict__ orig_of, const uint32_t* __restrict__ cell_start,
+                                 const GridParams& g, int k, NearHeap<KMAX>& t) {
     t.init();
     const int32_t cx = cell_coord(q.x, g.x0, g.inv, g.gw), cy = cell_coord(q.y, g.y0, g.inv, g.gh);
     const int32_t rmax = g.gw > g.gh ? g.gw : g.gh;
-    uint32_t found = 0;
     for (int32_t rho = 0; rho <= rmax; ++rho) {
-        if (rho >= 1 && found >= (uint32_t)k) {
+        if (rho >= 1 && t.size >= k) {
             const double lb = ((double)rho - 1.0 - 1e-6) * g.cs;
-            if (lb > 0 && lb * lb > t.d[k - 1]) break;
+            if (lb > 0 && lb * lb > t.d[0]) break;
         }
         const int32_t cnt = rho == 0 ? 1 : 8 * rho;
         for (int32_t c = 0; c < cnt; ++c) {
@@ -102,28 +126,11 @@ __device__ void knn_ring_search(uint32_t i, double2 q, const double2* __restrict
             if (x < 0 || y < 0 || x >= g.gw || y >= g.gh) continue;
             const uint32_t m = morton((uint32_t)x, (uint32_t)y);
             const uint32_t s = cell_start[m], e = cell_start[m + 1];
-            for (uint32_t jj = s; jj < e; ++jj) {
-                if (jj == i) continue;
-                ++found;
-                t.offer_lazy(dist2(q, xy[jj]), jj, orig_of, k);
-            }
+            for (uint32_t jj = s; jj < e; ++jj)
+                if (jj != i) t.offer(dist2(q, xy[jj]), jj, orig_of, k);
         }
     }
-}
-
-template <int KMAX>
-__device__ void knn_emit(uint32_t i, double2 q, const TopK<KMAX>& t, int kk, int k, const double2* __restrict__ xy,
-                         double beta, uint32_t* __restrict__ knn32, float* __restrict__ eta) {
-#pragma unroll
-    for (int r = 0; r < KMAX; ++r) {
-        const uint32_t jj = r < kk ? t.j[r] : kNone;
-        knn32[(size_t)i * KMAX + r] = jj;
-        if (r < k) {
-            int32_t d = euc2d(q, xy[jj]);
-            if (d < 1) d = 1;
-            eta[(size_t)i * k + r] = (float)power(beta, 1.0 / (double)d);
-        }
-    }
+    t.sort();
 }
 
 // One thread per city (internal id order, so a CTA covers a compact patch and its cell
@@ -140,9 +147,17 @@ __global__ void __launch_bounds__(128) k_knn_cells(const double2* __restrict__ x
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double2 q = xy[i];
-    TopK<KMAX> t;
-    knn_ring_search<KMAX>(i, q, xy, orig_of, cell_start, g, kk, t);
-    knn_emit<KMAX>(i, q, t, kk, k, xy, beta, knn32, eta);
+    NearHeap<KMAX> t;
+    near_ring_search<KMAX>(i, q, xy, orig_of, cell_start, g, kk, t);
+    for (int r = 0; r < KMAX; ++r) {
+        const uint32_t jj = r < kk ? t.j[r] : kNone;
+        knn32[(size_t)i * KMAX + r] = jj;
+        if (r < k) {
+            int32_t d = euc2d(q, xy[jj]);
+            if (d < 1) d = 1;
+            eta[(size_t)i * k + r] = (float)power(beta, 1.0 / (double)d);
+        }
+    }
 }
 
 // ============================================================ K5: weight table
@@ -173,7 +188,7 @@ __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ kn
     uint32_t c[KMAX];
     double acc[KMAX];
 #pragma unroll
-    for (int r = 0; r < KMAX; ++r) { c[r] = r < k ? knn32[(size_t)i * 32 + r] : kNone; acc[r] = 0.0; }
+    for (int r = 0; r < KMAX; ++r) { c[r] = r < k ? knn32[(size_t)i * kNearRow + r] : kNone; acc[r] = 0.0; }
     if (!T) {
         for (uint32_t a = 0; a < m; ++a) {
             const double ra = ratio[a];
@@ -199,7 +214,7 @@ __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ kn
 // ============================================================ K2: construction
 struct ConstructArgs {
     const uint2* cand;        // n*k {city, f32 weight}
-    const uint32_t* knn32;    // n*32 nearest cities by (d^2, orig), kNone padded
+    const uint32_t* knn32;    // n*kNearRow nearest cities by (d^2, orig), kNone padded
     const double2* xy;        // internal coordinates
     const uint32_t* orig_of;  // internal -> original (fallback tie-break)
     const uint32_t* int_of;   // original -> internal (start city draw)
@@ -366,11 +381,29 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_
                                                    uint32_t lane, uint32_t list_s, FbStats& fs) {
     const double2 q = ldg_d2(a.xy + cur);  // issued with the F0 row: F1 needs it first
     {
-        const uint32_t c = ldg_u32(&a.knn32[(size_t)cur * 32 + lane]);
-        const bool ok = c != kNone;
-        const uint32_t vw = lds_u32_if(vis_s + ((c >> 5) << 2), ok, ~0u);
-        const unsigned b = __ballot_sync(kFull, ok && !((vw >> (c & 31)) & 1u));
-        if (b) return __shfl_sync(kFull, c, __ffs(b) - 1);
+        // lane l holds entries [E*l, E*l + E) of the sorted near list; the first unvisited
+        // entry overall is one integer min-reduction over (entry index, city) keys
+        constexpr uint32_t E = kNearRow / 32;
+        uint32_t c[E];
+        const uint32_t* row = a.knn32 + (size_t)cur * kNearRow + E * lane;
+        if constexpr (E == 1) {
+            c[0] = ldg_u32(row);
+        } else if constexpr (E == 2) {
+            const uint2 v = ldg_u64(reinterpret_cast<const uint2*>(row));
+            c[0] = v.x; c[1] = v.y;
+        } else {
+            const uint4 v = ldg_u128(reinterpret_cast<const uint4*>(row));
+            c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+        }
+        uint32_t key = kNone;
+#pragma unroll
+        for (int s = E - 1; s >= 0; --s) {
+            const bool ok = c[s] != kNone;
+            const uint32_t vw = lds_u32_if(vis_s + ((c[s] >> 5) << 2), ok, ~0u);
+            if (ok && !((vw >> (c[s] & 31)) & 1u)) key = ((E * lane + s) << 21) | c[s];
+        }
+        const uint32_t km = __reduce_min_sync(kFull, key);
+        if (km != kNone) return km & 0x1fffffu;
     }
 #ifdef PACO_TIMING
     ++fs.searches;
@@ -838,7 +871,7 @@ __global__ void __launch_bounds__(256) k_classic(const uint32_t* __restrict__ kn
     const double keep = 1.0 - rho;
 #pragma unroll
     for (int r = 0; r < KMAX; ++r) {
-        c[r] = r < k ? knn32[(size_t)i * 32 + r] : kNone;
+        c[r] = r < k ? knn32[(size_t)i * kNearRow + r] : kNone;
         if (r < k) {
             double v = __dmul_rn(T[(size_t)i * k + r], keep);
             t[r] = v < 1e-6 ? 1e-6 : v;

@@ -266,7 +266,7 @@ static paco_status setup(paco_handle* h) {
     CU(dalloc(&keys, n)); CU(dalloc(&keys2, n)); CU(dalloc(&cellm, n));
     CU(dalloc(&h->cell_start, (size_t)h->g.ncells + 1));
     CU(dalloc(&h->sb_start, (size_t)(h->g.ncells >> 6) + 1));
-    CU(dalloc(&h->knn, (size_t)n * 32)); CU(dalloc(&h->eta, (size_t)n * k)); CU(dalloc(&h->cand, (size_t)n * h->kp));
+    CU(dalloc(&h->knn, (size_t)n * kNearRow)); CU(dalloc(&h->eta, (size_t)n * k)); CU(dalloc(&h->cand, (size_t)n * h->kp));
     CU(cudaMemsetAsync(h->cand, 0, sizeof(uint2) * (size_t)n * h->kp, st));
     if (h->mode == PACO_MODE_CLASSIC) {
         CU(dalloc(&h->T, (size_t)n * k));
@@ -297,8 +297,8 @@ static paco_status setup(paco_handle* h) {
     }
     CU(cudaGetLastError());
     // K1: k-NN lists, one thread per city, exact ring search over grid cells
-    const int kk = (int)std::min<uint32_t>(32, n - 1);
-    k_knn_cells<32><<<(n + 127) / 128, 128, 0, st>>>(h->xy, h->orig_of, h->cell_start, h->g, n, kk, (int)k,
+    const int kk = (int)std::min<uint32_t>(kNearRow, n - 1);
+    k_knn_cells<kNearRow><<<(n + 127) / 128, 128, 0, st>>>(h->xy, h->orig_of, h->cell_start, h->g, n, kk, (int)k,
                                                      h->cfg.beta, h->knn, h->eta);
     CU(cudaGetLastError());
     CU(cudaEventRecord(e1, st));
@@ -635,13 +635,13 @@ paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, u
     const uint32_t n = h->n, k = h->k;
     if (k_out) *k_out = k;
     std::vector<uint2> c((size_t)n * h->kp);
-    std::vector<uint32_t> kn((size_t)n * 32);
+    std::vector<uint32_t> kn((size_t)n * kNearRow);
     CU(cudaMemcpy(kn.data(), h->knn, sizeof(uint32_t) * kn.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(c.data(), h->cand, sizeof(uint2) * c.size(), cudaMemcpyDeviceToHost));
     for (uint32_t o = 0; o < n; ++o) {
         const uint32_t i = h->h_int[o];
         for (uint32_t r = 0; r < k; ++r) {
-            if (knn) knn[(size_t)o * k + r] = h->h_orig[kn[(size_t)i * 32 + r]];
+            if (knn) knn[(size_t)o * k + r] = h->h_orig[kn[(size_t)i * kNearRow + r]];
             if (weights) std::memcpy(&weights[(size_t)o * k + r], &c[(size_t)i * h->kp + r].y, 4);
         }
     }
