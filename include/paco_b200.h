@@ -7,9 +7,11 @@
  * with RunConfig at engine.hpp:42-76, RunReport at engine.hpp:84-92 and Mode at
  * engine.hpp:24. Its per-candidate plugin seam (PheromoneSource,
  * construction.hpp:236-241) is too fine-grained to cross a C ABI, so this
- * library replaces one whole synchronous iteration (engine.hpp:245-306) per
- * call: every ant constructs against a frozen colony on the GPU, then the
- * completion step applies l_best / g_best updates in ant order.
+ * library replaces whole iterations per call. Synchronous (engine.hpp:245-306):
+ * every ant constructs against a frozen colony on the GPU, then the completion
+ * step applies l_best / g_best updates in ant order. Asynchronous
+ * (engine.hpp:213-244, the reference's default): every ant runs its
+ * constructions back to back and applies its own updates at once.
  *
  * Conventions: plain pointers and sizes, no C++ types; every function returns a
  * paco_status (0 = ok); paco_last_error() returns a thread-local message. The
@@ -61,7 +63,7 @@ typedef struct paco_config {
     double max_mod_frac;           /* engine.hpp:48 */
     double two_opt_prob;           /* engine.hpp:49, first-improvement 2-opt after construction */
     uint32_t two_opt_window;       /* engine.hpp:50, 0 = unbounded (two_opt.hpp:33-35) */
-    uint32_t synchronous;          /* must be 1: the GPU engine is the barrier-sync path */
+    uint32_t synchronous;          /* engine.hpp:57; 0 = asynchronous (not with the reference rule) */
     uint64_t seed;
     double rho, tau_max, tau0;
     double time_budget_s;          /* 0 = run all iterations (engine.hpp:56) */
@@ -105,7 +107,8 @@ typedef struct paco_handle paco_handle;
 const char* paco_last_error(void);
 int paco_version(void);
 
-/* defaults of RunConfig (engine.hpp:42-59) with synchronous = 1, candidates = 16 */
+/* defaults of RunConfig (engine.hpp:42-59) except synchronous = 1 (deterministic per
+ * seed; the reference defaults to asynchronous), plus candidates = 16 */
 paco_status paco_config_default(paco_config* cfg);
 /* RunConfig::validate (engine.hpp:61-75) + classic n <= 5000 (engine.hpp:158-160) */
 paco_status paco_config_validate(const paco_config* cfg, uint32_t n, int mode);
@@ -115,8 +118,9 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
                         int mode, paco_handle** out);
 void paco_destroy(paco_handle* h);
 
-/* `count` synchronous iterations; the first iteration of a P-ACO run seeds every
- * l_best with a full construction (engine.hpp:290-292). */
+/* `count` iterations; the first iteration of a P-ACO run seeds every l_best with a
+ * full construction (engine.hpp:290-292). Asynchronous handles run them as one
+ * barrier-free launch in which each ant makes `count` constructions. */
 paco_status paco_iterate(paco_handle* h, uint64_t count);
 
 /* Validation mode: words for the NEXT iteration, m rows of `stride` u32 words

@@ -68,7 +68,7 @@ struct RunConfig {
     double tau0 = 1.0;
     double time_budget_s = 0.0;
     double convergence_interval_s = 1.0;
-    bool synchronous = true;  // the GPU engine runs barrier-synchronous iterations
+    bool synchronous = true;  // deterministic default; false = the reference's async engine (engine.hpp:213-244)
     bool validate_tours = false;
     std::uint32_t candidates = 16;  // k of the k-NN candidate list
     int device = -1;

@@ -171,14 +171,20 @@ template <int KMAX>
 __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ knn32, const float* __restrict__ eta,
                                                  const uint2* __restrict__ nbr, const int64_t* __restrict__ lb_len,
                                                  const uint8_t* __restrict__ has_lb, const int64_t* __restrict__ g_len,
+                                                 const unsigned long long* __restrict__ gkey,
                                                  const double* __restrict__ T, uint32_t n, uint32_t m, int k,
                                                  int kp, double alpha, double tau0, uint2* __restrict__ cand) {
     extern __shared__ double ratio[];
     if (!T) {
-        const double g = (double)*g_len;
+        // colony.hpp:159-177 ratios. In async mode (gkey != nullptr) the colony changes under
+        // this pass: lengths and g_best are read past L1 (ld.cv), a snapshot at pass start.
+        const double g = gkey ? (double)(long long)(__ldcv(gkey) >> 16) : (double)*g_len;
         for (uint32_t a = threadIdx.x; a < m; a += blockDim.x) {
             double r = 0.0;
-            if (has_lb[a]) { r = g / (double)lb_len[a]; r = r > 1.0 ? 1.0 : r; }
+            if (gkey ? __ldcv(reinterpret_cast<const unsigned char*>(&has_lb[a])) != 0 : has_lb[a] != 0) {
+                r = g / (double)(gkey ? __ldcv(reinterpret_cast<const long long*>(&lb_len[a])) : lb_len[a]);
+                r = r > 1.0 ? 1.0 : r;
+            }
             ratio[a] = r;
         }
         __syncthreads();
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ kn
         for (uint32_t a = 0; a < m; ++a) {
             const double ra = ratio[a];
             if (ra == 0.0) continue;
-            const uint2 p = __ldcs(&nbr[(size_t)a * n + i]);
+            const uint2 p = __ldcv(&nbr[(size_t)a * n + i]);  // streamed once; never a stale L1 copy
 #pragma unroll
             for (int r = 0; r < KMAX; ++r) {
                 if (c[r] == p.x) acc[r] = __dadd_rn(acc[r], ra);
@@ -564,11 +570,14 @@ __device__ __forceinline__ uint32_t last_unvisited(const uint32_t* vis, uint32_t
 //
 // KP = row stride (k rounded up to even; 0 = runtime value), STEPS = scan steps
 // (ceil(log2 k); extra steps never touch lanes < k), BUF = validation-buffer draws.
+// One construction of ant `ant` for iteration `iter` (the draw counter), seeding or not.
+// Returns the tour length (every lane); the tour is in the ant's non-l_best half.
+// cnt = {decisions, fallbacks, ties, forced, 2-opt runs}.
 template <int KP, int STEPS, bool BUF>
-__global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];  // fallback list | visited bitmap | warm scratch
+__device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t ant, uint64_t iter, bool seeding,
+                                               unsigned char* smem_raw, const FallbackCtx& fctx, bool& partial_out,
+                                               uint32_t (&cnt)[5]) {
     const uint32_t lane = threadIdx.x;
-    const uint32_t ant = a.force ? a.force_ant : blockIdx.x;
     const uint32_t n = a.n, k = a.k, nw = a.nwords;
     const uint32_t kp = KP ? (uint32_t)KP : a.kp;
     uint32_t* fb_list = reinterpret_cast<uint32_t*>(smem_raw);
@@ -577,11 +586,9 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     const uint32_t* wrow = BUF ? a.words + (a.force ? 0 : (uint64_t)ant * a.stride) : nullptr;
     auto word = [&](uint32_t slot) -> uint32_t {
         if (BUF) return wrow[slot];
-        const uint4 v = philox10(make_uint4(slot >> 2, ant, (uint32_t)a.iter, (uint32_t)(a.iter >> 32)), key);
+        const uint4 v = philox10(make_uint4(slot >> 2, ant, (uint32_t)iter, (uint32_t)(iter >> 32)), key);
         return pick_word(v, slot & 3);
     };
-    __shared__ FallbackCtx fctx;
-    if (lane == 0) { fctx.knn32 = a.knn32; fctx.xy = a.xy; fctx.orig_of = a.orig_of; fctx.sb_start = a.sb_start; fctx.g = a.g; }
     for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
     __syncwarp();
     if (lane == 0 && (n & 31)) vis[nw - 1] = 0xffffffffu << (n & 31);  // padding bits count as visited
@@ -592,7 +599,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     bool partial = false;
     uint32_t start_pos = 0, m_mod = 0;
     if (a.force) { partial = true; start_pos = a.force_start_pos; m_mod = a.force_m_mod; }
-    else if (!a.seeding) {
+    else if (!seeding) {
         partial = u01_f64(word(0)) < a.eff_pp;  // engine.hpp:137-138
         if (partial) {
             start_pos = below(word(1), n);       // construction.hpp:358
@@ -638,7 +645,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     // lanes >= k never load: they hold (cur, 0.0f), and cur is always marked visited
     const bool lane_in = lane < k;
     const uint2* __restrict__ row_base = a.cand + lane;
-    const uint32_t iter_lo = (uint32_t)a.iter, iter_hi = (uint32_t)(a.iter >> 32);
+    const uint32_t iter_lo = (uint32_t)iter, iter_hi = (uint32_t)(iter >> 32);
     FbStats fs;
 #ifdef PACO_TIMING
     const long long loop0 = clock64();
@@ -799,25 +806,128 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
         }
         if (__any_sync(kFull, bad) && lane == 0) atomicExch(a.err, 1);
     }
-    if (lane == 0) {
+    partial_out = partial;
+    cnt[0] = n_dec; cnt[1] = n_fb; cnt[2] = n_tie; cnt[3] = n_forced; cnt[4] = n_2opt;
+    return len;
+}
+
+__device__ __forceinline__ void init_fallback_ctx(const ConstructArgs& a, FallbackCtx& fctx) {
+    if (threadIdx.x == 0) {
+        fctx.knn32 = a.knn32; fctx.xy = a.xy; fctx.orig_of = a.orig_of; fctx.sb_start = a.sb_start; fctx.g = a.g;
+    }
+    __syncwarp();
+}
+
+// Synchronous construction: every ant once against the frozen colony (engine.hpp:245-306);
+// the completion step (k_update, k_publish) runs after it in ant order.
+template <int KP, int STEPS, bool BUF>
+__global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];  // fallback list | visited bitmap | warm scratch
+    __shared__ FallbackCtx fctx;
+    init_fallback_ctx(a, fctx);
+    const uint32_t ant = a.force ? a.force_ant : blockIdx.x;
+    bool partial;
+    uint32_t cnt[5];
+    const long long len = build_one<KP, STEPS, BUF>(a, ant, a.iter, a.seeding != 0, smem_raw, fctx, partial, cnt);
+    if (threadIdx.x == 0) {
         a.new_len[ant] = len;
         if (!a.force) {
             a.partial_flag[ant] = partial ? 1 : 0;
-            atomicAdd(&a.counters[0], (unsigned long long)n_dec);
-            atomicAdd(&a.counters[1], (unsigned long long)n_fb);
-            atomicAdd(&a.counters[2], (unsigned long long)n_tie);
-            atomicAdd(&a.counters[3], (unsigned long long)n_forced);
+            atomicAdd(&a.counters[0], (unsigned long long)cnt[0]);
+            atomicAdd(&a.counters[1], (unsigned long long)cnt[1]);
+            atomicAdd(&a.counters[2], (unsigned long long)cnt[2]);
+            atomicAdd(&a.counters[3], (unsigned long long)cnt[3]);
             atomicAdd(&a.counters[partial ? 5 : 4], 1ull);
-            if (n_2opt) atomicAdd(&a.counters[9], 1ull);
+            if (cnt[4]) atomicAdd(&a.counters[9], 1ull);
         }
     }
+}
+
+// Colony state the asynchronous mode updates from inside the construction kernel.
+struct AsyncState {
+    uint2* nbr;                   // m*n published (prev, next) of every l_best
+    int64_t* lb_len;
+    uint8_t* has_lb;
+    uint8_t* lb_sel;
+    unsigned long long* gkey;     // g_best as (length << 16 | ant), atomicMin
+    uint8_t* improved;            // of the ant's latest construction (readback)
+};
+
+// Asynchronous mode (engine.hpp:213-244, the reference's default): each ant's warp runs
+// `count` constructions back to back with no barrier and applies its own update
+// immediately - update_l_best (strict improvement, colony.hpp:117-124) with the
+// publish of its neighbour slice (colony.hpp:39-52), then update_g_best
+// (colony.hpp:127-139) as an atomic minimum. The candidate weights are rebuilt by
+// k_weights passes running concurrently on another stream, so constructions see other
+// ants' improvements with a delay, as the reference's workers see them whenever they
+// next gather. Not deterministic (the reference's async mode is not either).
+template <int KP, int STEPS>
+__global__ void __launch_bounds__(32, 1) k_construct_async(ConstructArgs a, uint32_t count, AsyncState st) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ FallbackCtx fctx;
+    init_fallback_ctx(a, fctx);
+    const uint32_t lane = threadIdx.x, ant = blockIdx.x, n = a.n;
+    unsigned long long tot[5] = {0, 0, 0, 0, 0}, fulls = 0, parts = 0, imps = 0;
+    for (uint32_t it = 0; it < count; ++it) {
+        bool partial;
+        uint32_t cnt[5];
+        const long long len = build_one<KP, STEPS, false>(a, ant, a.iter + it, a.seeding != 0 && it == 0, smem_raw,
+                                                          fctx, partial, cnt);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) tot[q] += cnt[q];
+        if (partial) ++parts; else ++fulls;
+        const bool imp = !st.has_lb[ant] || len < st.lb_len[ant];
+        if (lane == 0) {
+            a.new_len[ant] = len;
+            a.partial_flag[ant] = partial ? 1 : 0;
+            st.improved[ant] = imp ? 1 : 0;
+        }
+        if (imp) {
+            const uint8_t ns = (uint8_t)(1 - st.lb_sel[ant]);
+            const uint32_t* t = a.tours + ((size_t)ant * 2 + ns) * n;
+            uint2* nb = st.nbr + (size_t)ant * n;
+            for (uint32_t p = lane; p < n; p += 32)
+                nb[t[p]] = make_uint2(t[p == 0 ? n - 1 : p - 1], t[p + 1 == n ? 0 : p + 1]);
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();  // the slice before the length that makes it count
+                st.lb_sel[ant] = ns;
+                st.has_lb[ant] = 1;
+                *(volatile int64_t*)&st.lb_len[ant] = len;
+                __threadfence();
+                atomicMin(st.gkey, ((unsigned long long)len << 16) | ant);
+            }
+            ++imps;
+            __syncwarp();
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) atomicAdd(&a.counters[q], tot[q]);
+        atomicAdd(&a.counters[9], tot[4]);
+        atomicAdd(&a.counters[4], fulls);
+        atomicAdd(&a.counters[5], parts);
+        atomicAdd(&a.counters[7], imps);
+    }
+}
+
+// g_best between the two encodings: the sync path's GBest, the async path's atomic key
+struct GBest { long long len; int32_t ant; int32_t has; };
+__global__ void k_gkey_from_gbest(const GBest* __restrict__ gb, unsigned long long* __restrict__ gkey) {
+    *gkey = gb->has ? (((unsigned long long)gb->len << 16) | (uint32_t)gb->ant) : ~0ull;
+}
+__global__ void k_gbest_from_gkey(const unsigned long long* __restrict__ gkey, GBest* __restrict__ gb,
+                                  int64_t* __restrict__ g_len) {
+    const unsigned long long k = *gkey;
+    if (k == ~0ull) return;
+    gb->len = (long long)(k >> 16); gb->ant = (int32_t)(k & 0xffffu); gb->has = 1;
+    *g_len = (int64_t)(k >> 16);
 }
 
 // ============================================================ K4: completion step
 // engine.hpp:261-265: for every ant in order, update_l_best (strict improvement,
 // colony.hpp:117-124) then update_g_best (colony.hpp:127-139). The l_best switch is
 // a flip of the ant's double-buffer selector, so no tour is copied.
-struct GBest { long long len; int32_t ant; int32_t has; };
 
 __global__ void k_update(uint32_t first, uint32_t count, const int64_t* __restrict__ new_len,
                          int64_t* __restrict__ lb_len, uint8_t* __restrict__ has_lb, uint8_t* __restrict__ lb_sel,

@@ -70,6 +70,9 @@ struct paco_handle {
     uint2* cur_nbr = nullptr;
     double* T = nullptr;
     GBest* gb = nullptr;
+    unsigned long long* gkey = nullptr;  // async mode: g_best as (length << 16 | ant)
+    cudaStream_t st2 = nullptr;          // async mode: concurrent weight rebuilds
+    bool async_mode = false;
     unsigned long long* counters = nullptr;
     int* err = nullptr;
     uint32_t* words = nullptr;
@@ -77,7 +80,7 @@ struct paco_handle {
     bool words_ready = false;
     uint32_t* scratch_u32 = nullptr;  // n-sized staging for offers / construct_at
     unsigned long long* scratch_u64 = nullptr;
-    uint64_t iter = 0;
+    uint64_t iter = 0, weight_passes = 0;
     double construct_ms = 0, update_ms = 0, setup_ms = 0;
     std::vector<cudaEvent_t> evpool;
     // reference-rule (IR) mode
@@ -89,12 +92,13 @@ struct paco_handle {
     ~paco_handle() {
         if (dev >= 0) cudaSetDevice(dev);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
-                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, counters, err, words,
+                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words,
                         scratch_u32, scratch_u64, rng, ratio, Tfull};
         for (void* p : ptrs)
             if (p) cudaFree(p);
         for (auto e : evpool) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
+        if (st2) cudaStreamDestroy(st2);
     }
 };
 
@@ -111,7 +115,7 @@ paco_status paco_config_default(paco_config* c) {
     c->partial_prob = 0.95; c->max_mod_frac = 1.0; c->two_opt_prob = 0.0; c->two_opt_window = 0;
     c->workers = 8; c->seed = 1; c->rho = 0.1; c->tau_max = 1.0; c->tau0 = 1.0;
     c->time_budget_s = 0.0; c->convergence_interval_s = 1.0;
-    c->synchronous = 1;  // the reference default is async; the GPU engine is the sync path
+    c->synchronous = 1;  // the reference defaults to async; the GPU engine defaults to the deterministic path
     c->validate_tours = 0;
     c->candidates = 16; c->draws = PACO_DRAWS_PHILOX; c->device = -1;
     return PACO_OK;
@@ -143,7 +147,12 @@ paco_status paco_config_validate(const paco_config* c, uint32_t n, int mode) {
     if (c->rule > 1) return fail(PACO_E_INVALID, "unknown selection rule");
     if (c->rule == PACO_RULE_INDEPENDENT_ROULETTE && c->draws != PACO_DRAWS_PHILOX)
         return fail(PACO_E_INVALID, "the reference rule draws from its own xoshiro256++ streams");
-    if (!c->synchronous) return fail(PACO_E_UNSUPPORTED, "asynchronous mode is not provided by the GPU engine yet");
+    // classic mode always runs barriered iterations (engine.hpp:213); the reference rule is
+    // kept synchronous, its purpose being bit-identity with paco::run
+    if (!c->synchronous && mode != PACO_MODE_CLASSIC && c->rule == PACO_RULE_INDEPENDENT_ROULETTE)
+        return fail(PACO_E_UNSUPPORTED, "the reference-rule engine is synchronous only");
+    if (!c->synchronous && mode != PACO_MODE_CLASSIC && c->ants > 65535)
+        return fail(PACO_E_UNSUPPORTED, "asynchronous mode supports at most 65535 ants");
     return PACO_OK;
 }
 
@@ -189,7 +198,7 @@ static paco_status alloc_colony(paco_handle* h) {
     CU(dalloc(&h->lb_sel, m)); CU(dalloc(&h->has_lb, m)); CU(dalloc(&h->improved, m)); CU(dalloc(&h->partial, m));
     CU(dalloc(&h->new_len, m)); CU(dalloc(&h->lb_len, m)); CU(dalloc(&h->g_len, 1));
     CU(dalloc(&h->nbr, (size_t)m * n));
-    CU(dalloc(&h->gb, 1)); CU(dalloc(&h->counters, 16)); CU(dalloc(&h->err, 1));
+    CU(dalloc(&h->gb, 1)); CU(dalloc(&h->gkey, 1)); CU(dalloc(&h->counters, 16)); CU(dalloc(&h->err, 1));
     CU(dalloc(&h->scratch_u32, (size_t)n + 64)); CU(dalloc(&h->scratch_u64, 4));
     CU(cudaMemsetAsync(h->lb_sel, 0, m, st)); CU(cudaMemsetAsync(h->has_lb, 0, m, st));
     CU(cudaMemsetAsync(h->improved, 0, m, st)); CU(cudaMemsetAsync(h->partial, 0, m, st));
@@ -356,6 +365,22 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
         delete h;
         return fail(PACO_E_CUDA, "stream creation failed");
     }
+    h->async_mode = !cfg->synchronous && mode != PACO_MODE_CLASSIC;
+    if (h->async_mode) {
+        // g_best key packs the length into 48 bits: bound it by n x the bounding-box diagonal
+        double x0 = xs[0], x1 = xs[0], y0 = ys[0], y1 = ys[0];
+        for (uint32_t i = 1; i < n; ++i) {
+            x0 = std::min(x0, xs[i]); x1 = std::max(x1, xs[i]); y0 = std::min(y0, ys[i]); y1 = std::max(y1, ys[i]);
+        }
+        if ((double)n * (std::sqrt((x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0)) + 1.0) >= 0x1p48) {
+            delete h;
+            return fail(PACO_E_UNSUPPORTED, "asynchronous mode needs tour lengths below 2^48");
+        }
+        if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess) {
+            delete h;
+            return fail(PACO_E_CUDA, "stream creation failed");
+        }
+    }
     s = setup(h);
     if (s != PACO_OK) { delete h; return s; }
     *out = h;
@@ -373,8 +398,9 @@ static cudaEvent_t ev(paco_handle* h, size_t i) {
     return h->evpool[i];
 }
 
-static paco_status launch_weights(paco_handle* h) {
+static paco_status launch_weights(paco_handle* h, cudaStream_t stream = nullptr, const unsigned long long* gkey = nullptr) {
     const uint32_t n = h->n, tb = 256;
+    if (!stream) stream = h->st;
     const size_t smem = h->T ? 0 : sizeof(double) * h->m;
     const int km = kmax_for(h->k);
     const double* T = h->mode == PACO_MODE_CLASSIC ? h->T : nullptr;
@@ -382,9 +408,9 @@ static paco_status launch_weights(paco_handle* h) {
     do {                                                                                                   \
         if (smem > 48 * 1024)                                                                              \
             CU(cudaFuncSetAttribute(k_weights<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        k_weights<KM><<<(n + tb - 1) / tb, tb, smem, h->st>>>(h->knn, h->eta, h->nbr, h->lb_len, h->has_lb,  \
-                                                            h->g_len, T, n, h->m, (int)h->k, (int)h->kp, h->cfg.alpha, \
-                                                            h->cfg.tau0, h->cand);                         \
+        k_weights<KM><<<(n + tb - 1) / tb, tb, smem, stream>>>(h->knn, h->eta, h->nbr, h->lb_len, h->has_lb,  \
+                                                            h->g_len, gkey, T, n, h->m, (int)h->k, (int)h->kp,  \
+                                                            h->cfg.alpha, h->cfg.tau0, h->cand);           \
     } while (0)
     if (km == 8) LAUNCH_W(8); else if (km == 16) LAUNCH_W(16); else if (km == 24) LAUNCH_W(24); else LAUNCH_W(32);
 #undef LAUNCH_W
@@ -461,6 +487,65 @@ static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint
     return buf ? launch(k_construct<0, 5, true>) : launch(k_construct<0, 5, false>);
 }
 
+static paco_status launch_construct_async(paco_handle* h, const ConstructArgs& a, uint32_t count) {
+    const size_t smem = kFbList * 4 + (size_t)h->nwords * 4 + 512 + 16;
+    const int per_sm = (int)((h->m + h->num_sms - 1) / h->num_sms);
+    const int carve = (int)std::min<size_t>(100, (size_t)per_sm * (smem + 1024) * 100 / (228 * 1024) + 1);
+    const AsyncState st{h->nbr, h->lb_len, h->has_lb, h->lb_sel, h->gkey, h->improved};
+    auto launch = [&](auto kern) -> paco_status {
+        if (smem > 48 * 1024)
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+        kern<<<h->m, 32, smem, h->st>>>(a, count, st);
+        CU(cudaGetLastError());
+        return PACO_OK;
+    };
+    if (h->kp == 16) return launch(k_construct_async<16, 4>);
+    if (h->kp == 20) return launch(k_construct_async<20, 5>);
+    return launch(k_construct_async<0, 5>);
+}
+
+static paco_status check_err(paco_handle* h);
+
+// Asynchronous iterations (engine.hpp:213-244): one persistent launch in which every ant
+// runs `count` constructions with immediate updates, while k_weights passes rebuild the
+// candidate weights from the live colony on a second stream until it finishes.
+static paco_status iterate_async(paco_handle* h, uint64_t count) {
+    if (count == 0) return PACO_OK;
+    if (count > 0xffffffffull) return fail(PACO_E_INVALID, "too many iterations for one call");
+    const bool seeding = h->iter == 0;
+    k_gkey_from_gbest<<<1, 1, 0, h->st>>>(h->gb, h->gkey);
+    CU(cudaGetLastError());
+    paco_status s = launch_weights(h, h->st, h->gkey);
+    if (s != PACO_OK) return s;
+    cudaEvent_t e0 = ev(h, 0), e1 = ev(h, 1);
+    CU(cudaEventRecord(e0, h->st));
+    s = launch_construct_async(h, construct_args(h, seeding), (uint32_t)count);
+    if (s != PACO_OK) return s;
+    CU(cudaEventRecord(e1, h->st));
+    uint64_t passes = 0;
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(e1);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) return fail(PACO_E_CUDA, cudaGetErrorString(q));
+        s = launch_weights(h, h->st2, h->gkey);
+        if (s != PACO_OK) return s;
+        CU(cudaStreamSynchronize(h->st2));
+        ++passes;
+    }
+    k_gbest_from_gkey<<<1, 1, 0, h->st>>>(h->gkey, h->gb, h->g_len);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(h->st));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    h->construct_ms = ms;
+    h->update_ms = 0.0;  // the updates run inside the construction kernel
+    h->weight_passes += passes;
+    h->iter += count;
+    if (h->cfg.validate_tours) return check_err(h);
+    return PACO_OK;
+}
+
 static paco_status check_err(paco_handle* h) {
     int err = 0;
     CU(cudaMemcpyAsync(&err, h->err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
@@ -474,6 +559,11 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
     CU(cudaSetDevice(h->dev));
     if (h->cfg.draws == PACO_DRAWS_BUFFER && count > 1)
         return fail(PACO_E_INVALID, "buffer draws feed one iteration per paco_set_draws call");
+    if (h->async_mode) {
+        if (h->cfg.draws == PACO_DRAWS_BUFFER)
+            return fail(PACO_E_INVALID, "validation (buffer) draws need synchronous iterations");
+        return iterate_async(h, count);
+    }
     const uint32_t n = h->n, m = h->m;
     std::vector<std::pair<size_t, size_t>> marks;
     size_t e = 0;

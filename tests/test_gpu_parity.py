@@ -11,7 +11,7 @@ import pytest
 import oracle
 from paper_1709_03187_b200 import (Colony, InvalidArgument, Mode, PacoError, RunConfig, cycle_length,
                                    grid_instance, is_permutation_of_n, make_config_instance, run)
-from paper_1709_03187_b200.instances import Instance
+from paper_1709_03187_b200.instances import CONFIGS, Instance
 
 pytestmark = pytest.mark.gpu
 
@@ -238,7 +238,39 @@ def test_config_errors():
     with pytest.raises(InvalidArgument):
         Colony(inst, RunConfig(ants=0))
     with pytest.raises(PacoError):
-        Colony(inst, RunConfig(ants=4, synchronous=False))
+        Colony(inst, RunConfig(ants=4, synchronous=False, rule="independent"))
+
+
+@pytest.mark.parametrize("cfgname,iters,p2", [("C1", 100, 0.0), ("C2", 12, 0.0), ("C1", 40, 0.05)])
+def test_async_mode(cfgname, iters, p2):
+    """f3, the reference's default engine (engine.hpp:213-244): ants run their constructions with
+    no barrier and update l_best / g_best immediately. Not deterministic, so checked by
+    invariants: every tour a permutation with its exact length (validate_tours), l_best never
+    worse than the last tour, g_best = min over l_best and held by a permutation, build counts,
+    and quality within 3% of the synchronous engine at the same seed."""
+    spec = CONFIGS[cfgname]
+    inst = make_config_instance(cfgname)
+    res = {}
+    for sync in (True, False):
+        cfg = RunConfig(ants=spec["m"], alpha=1.0, beta=2.0, candidates=spec["k"], seed=7, synchronous=sync,
+                        validate_tours=True, two_opt_prob=p2, two_opt_window=20)
+        with Colony(inst, cfg) as col:
+            col.iterate(1)
+            col.iterate(iters - 1)
+            c = col.counters()
+            assert c["iterations"] == iters
+            assert c["full_builds"] + c["partial_builds"] == spec["m"] * iters
+            assert c["improvements"] >= spec["m"]
+            t, l = col.tours()
+            lt, ll = col.l_best()
+            g, gl = col.g_best()
+            for a in range(spec["m"]):
+                assert is_permutation_of_n(inst.n, t[a]) and cycle_length(inst, t[a]) == l[a]
+                assert is_permutation_of_n(inst.n, lt[a]) and cycle_length(inst, lt[a]) == ll[a]
+                assert ll[a] <= l[a]
+            assert gl == ll.min() and cycle_length(inst, g) == gl
+            res[sync] = gl
+    assert abs(res[False] - res[True]) <= 0.03 * res[True]
 
 
 def test_cpp_drop_in_on_gpu(tmp_path):

@@ -156,8 +156,13 @@ def test_classic_size_limit_and_unsupported(native):
         RunConfig().validate(n=5001, mode=Mode.classic_aco)
     RunConfig().validate(n=5000, mode=Mode.classic_aco)
     RunConfig(two_opt_prob=0.1, two_opt_window=500).validate()  # f2: supported
+    RunConfig(synchronous=False).validate()  # f3: the reference's default async engine
+    RunConfig(synchronous=False).validate(mode=Mode.classic_aco)  # classic runs barriered anyway
     with pytest.raises(PacoError) as ei:
-        RunConfig(synchronous=False).validate()
+        RunConfig(synchronous=False, rule="independent").validate()
+    assert ei.value.status == N.PACO_E_UNSUPPORTED
+    with pytest.raises(PacoError) as ei:
+        RunConfig(synchronous=False, ants=70000).validate()
     assert ei.value.status == N.PACO_E_UNSUPPORTED
 
 
