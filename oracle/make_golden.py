@@ -135,6 +135,117 @@ def main() -> None:
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
+    bench_fixtures()
+
+
+BENCH_OUT = os.path.join(ROOT, "tests", "golden", "bench_golden.json")
+
+# scripts for oracle/ref_bench_tool (rows mode): ROW label instance mode iterations max_mod pp
+# two_opt_prob window pairing error|- ; REC instance row trial seed best pct_error wall_s
+# iterations comparisons ; AGG ; SPEEDUP i j ; LABEL mode max_mod pp two_opt_prob
+BENCH_SCRIPTS = [
+    """ROW table4 pcb442 paco 100000 1 1 0 0 equal_iterations -
+REC pcb442 baseline 0 1000 50903 0.21653543307086615 12.5 100000 160000000
+REC pcb442 baseline 1 1001 50850 0.11220472440944881 12.25 100000 160000000
+REC pcb442 baseline 2 1002 51002 0.41141732283464566 13.125 100000 160000000
+ROW table4 pcb442 partial 100000 0.5 0.95 0 0 equal_iterations -
+REC pcb442 partial_mm0.5_pp0.95_ls0 0 1000 50990 0.38779527559055116 3.1 100000 41000000
+REC pcb442 partial_mm0.5_pp0.95_ls0 1 1001 50779 -0.027559055118110236 2.9 100000 40000000
+REC pcb442 partial_mm0.5_pp0.95_ls0 2 1002 51204 0.80708661417322836 3.30000000001 100000 42000000
+ROW table4 pcb442 partial 100000 0.1 0.95 0.001 500 equal_iterations boom
+REC pcb442 partial_mm0.1_pp0.95_ls0.001 0 1000 50779 0 0.1 100000 7
+AGG
+SPEEDUP 1 0
+SPEEDUP 2 0
+LABEL partial 0.5 0.95 0
+LABEL partial 0.1 1 0.001
+LABEL paco 0.30000000000000004 0.95 1e-07
+LABEL classic 1 1 0.33333333333333331
+""",
+    """ROW t8 earring200K partial 500 0.01 1 0.001 500 time_budget -
+REC earring200K partial_mm0.01_pp1_ls0.001 0 1000 7990000 nan 3600.5 500 99999999999
+REC earring200K partial_mm0.01_pp1_ls0.001 1 1001 7980000 nan 3599.75 500 88888888888
+ROW t8 earring200K paco_timed 500 1 1 0 0 time_budget -
+REC earring200K timed_baseline 0 8777 8100000 nan 3600.5 37 11111111111
+REC earring200K timed_baseline 1 8778 8090000 nan 3599.75 41 22222222222
+ROW t8 other partial 499 1 1 0 0 equal_iterations -
+AGG
+SPEEDUP 0 1
+SPEEDUP 0 2
+SPEEDUP 2 0
+LABEL partial 0.01 1 0.001
+""",
+    """ROW solo x.tsp partial 7 1 1 0 3 equal_iterations -
+REC x a 0 5 123 1e-20 1e-300 7 0
+AGG
+""",
+]
+
+BENCH_CONFIGS = [
+    """# full experiment
+label = "sweep one"   # quoted
+instances = ["data/a.tsp", "data/b c.tsp"]
+optima = data/optima.txt
+mode = partial
+trials = 5
+ants = 32
+iterations = 2000
+alpha = 1.5
+beta = 2
+workers = 4
+seed = 77
+rho = 0.25
+tau_max = 2.5
+tau0 = 0.5
+two_opt_window = 50
+convergence_interval = 0.5
+synchronous = true
+validate_tours = false
+baseline = false
+timed_baseline = true
+out_dir = out/run1
+max_mod = [0.5, 0.25, 0.1]
+partial_prob = [1.0, 0.95]
+two_opt_prob = [0.0, 0.001]
+""",
+    "mode = paco\nmax_mod = []\n",
+    "alpha = 1.5abc\ntrials = 12x\n",
+    "trials = -1\n",
+    "label = x\nnot a key value\n",
+    "bogus = 3\n",
+    "alpha = fast\n",
+    "baseline = yes\n",
+    "max_mod = [0.5, 0.2\n",
+    "label = \"open\n",
+    "alpha = [1, 2]\n",
+    "alpha = 1, 2\n",
+    "mode = turbo\n",
+    "max_mod = [0.5, x]\n",
+    "trials = \n",
+    "   \n# only comments\n\n",
+]
+
+BENCH_PRESETS = ["table1", "table2", "table3", "table4", "table5", "table6", "table7", "table8", "table9"]
+
+
+def bench_fixtures() -> None:
+    import json
+    import subprocess
+
+    tool = os.path.join(HERE, "_ref", "ref_bench_tool")
+    out = {"rows": [], "config": [], "preset": []}
+    for sc in BENCH_SCRIPTS:
+        r = subprocess.run([tool, "rows"], input=sc, capture_output=True, text=True, check=True)
+        out["rows"].append({"input": sc, "output": r.stdout})
+    for cf in BENCH_CONFIGS:
+        r = subprocess.run([tool, "config"], input=cf, capture_output=True, text=True, check=True)
+        out["config"].append({"input": cf, "output": r.stdout})
+    for name in BENCH_PRESETS:
+        r = subprocess.run([tool, "preset", name], capture_output=True, text=True, check=True)
+        out["preset"].append({"input": name, "output": r.stdout})
+    with open(BENCH_OUT, "w") as f:
+        json.dump(out, f, indent=1)
+    print(f"wrote {BENCH_OUT}")
 
 
 if __name__ == "__main__":
