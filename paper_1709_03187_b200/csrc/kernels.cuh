@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(128) k_knn_cells(const double2* __restrict__ x
 // edges; ratios per colony.hpp:159-177), w = f32(Power(alpha)(tau)) * eta^beta (f32).
 // Classic mode reads tau from the candidate-edge pheromone table T instead.
 // Output: packed {c_r, w} rows, the only table the construction kernel reads.
-template <int KMAX>
+template <int KMAX, bool LIVE>
 __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ knn32, const float* __restrict__ eta,
                                                  const uint2* __restrict__ nbr, const int64_t* __restrict__ lb_len,
                                                  const uint8_t* __restrict__ has_lb, const int64_t* __restrict__ g_len,
@@ -196,14 +196,28 @@ __global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ kn
 #pragma unroll
     for (int r = 0; r < KMAX; ++r) { c[r] = r < k ? knn32[(size_t)i * kNearRow + r] : kNone; acc[r] = 0.0; }
     if (!T) {
-        for (uint32_t a = 0; a < m; ++a) {
-            const double ra = ratio[a];
-            if (ra == 0.0) continue;
-            const uint2 p = __ldcv(&nbr[(size_t)a * n + i]);  // streamed once; never a stale L1 copy
+        // eight ants' pairs in flight per thread, then accumulated in ant order (the fp64 sum
+        // order of ColonyPheromone::begin_step). The slices are streamed once: evict-first in
+        // sync mode, read past L1 in async mode (LIVE), where ants rewrite them meanwhile.
+        constexpr uint32_t U = 8;
+        for (uint32_t a0 = 0; a0 < m; a0 += U) {
+            uint2 p[U];
+            double rr[U];
 #pragma unroll
-            for (int r = 0; r < KMAX; ++r) {
-                if (c[r] == p.x) acc[r] = __dadd_rn(acc[r], ra);
-                if (c[r] == p.y) acc[r] = __dadd_rn(acc[r], ra);
+            for (uint32_t u = 0; u < U; ++u) {
+                const uint32_t a = a0 + u;
+                rr[u] = a < m ? ratio[a] : 0.0;
+                const uint2* src = &nbr[(size_t)a * n + i];
+                p[u] = rr[u] != 0.0 ? (LIVE ? __ldcv(src) : __ldcs(src)) : make_uint2(kNone, kNone);
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+                if (rr[u] == 0.0) continue;
+#pragma unroll
+                for (int r = 0; r < KMAX; ++r) {
+                    if (c[r] == p[u].x) acc[r] = __dadd_rn(acc[r], rr[u]);
+                    if (c[r] == p[u].y) acc[r] = __dadd_rn(acc[r], rr[u]);
+                }
             }
         }
     }

@@ -404,16 +404,18 @@ static paco_status launch_weights(paco_handle* h, cudaStream_t stream = nullptr,
     const size_t smem = h->T ? 0 : sizeof(double) * h->m;
     const int km = kmax_for(h->k);
     const double* T = h->mode == PACO_MODE_CLASSIC ? h->T : nullptr;
-#define LAUNCH_W(KM)                                                                                       \
+#define LAUNCH_W2(KM, LIVE)                                                                                \
     do {                                                                                                   \
         if (smem > 48 * 1024)                                                                              \
-            CU(cudaFuncSetAttribute(k_weights<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        k_weights<KM><<<(n + tb - 1) / tb, tb, smem, stream>>>(h->knn, h->eta, h->nbr, h->lb_len, h->has_lb,  \
-                                                            h->g_len, gkey, T, n, h->m, (int)h->k, (int)h->kp,  \
-                                                            h->cfg.alpha, h->cfg.tau0, h->cand);           \
+            CU(cudaFuncSetAttribute(k_weights<KM, LIVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        k_weights<KM, LIVE><<<(n + tb - 1) / tb, tb, smem, stream>>>(h->knn, h->eta, h->nbr, h->lb_len,       \
+                                                            h->has_lb, h->g_len, gkey, T, n, h->m, (int)h->k,  \
+                                                            (int)h->kp, h->cfg.alpha, h->cfg.tau0, h->cand);   \
     } while (0)
+#define LAUNCH_W(KM) do { if (gkey) LAUNCH_W2(KM, true); else LAUNCH_W2(KM, false); } while (0)
     if (km == 8) LAUNCH_W(8); else if (km == 16) LAUNCH_W(16); else if (km == 24) LAUNCH_W(24); else LAUNCH_W(32);
 #undef LAUNCH_W
+#undef LAUNCH_W2
     CU(cudaGetLastError());
     return PACO_OK;
 }
