@@ -274,33 +274,21 @@ struct FbStats {
 #endif
 };
 
-__device__ __forceinline__ uint2 lds_u64(uint32_t addr) {
-    uint2 v;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
-    return v;
-}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
-}
-__device__ __forceinline__ void red_or_shared(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 __device__ __forceinline__ void sts_u32_if(uint32_t addr, uint32_t v, bool cond) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
                  "r"((uint32_t)cond)
                  : "memory");
 }
-__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
-}
 // predicated 16-byte global->shared async copy (LDGSTS), L1-allocating
 __device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, bool cond) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 16;\n\t}" ::"r"(dst),
                  "l"(src), "r"((uint32_t)cond));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 constexpr uint32_t kFbList = 256;  // per-warp shared-memory list of unvisited city ids (fallback)
@@ -563,11 +551,6 @@ __device__ __forceinline__ uint32_t last_unvisited(const uint32_t* vis, uint32_t
     return kNone;
 }
 
-#ifdef PACO_TIMING
-#define PACO_CLOCK(var, dep) long long var; asm volatile("mov.u64 %0, %%clock64;" : "=l"(var) : "r"(dep))
-#else
-#define PACO_CLOCK(var, dep)
-#endif
 
 // One warp per ant (construction.hpp:283-365 with the north-star selection rule,
 // engine.hpp:129-148 draw order). The visited bitmap (n bits) lives in shared
