@@ -57,22 +57,25 @@ __global__ void k_sb_start(const uint32_t* __restrict__ cell_start, uint32_t nsb
 // Per city: the k nearest other cities by (d^2, original index), rows in internal
 // ids; eta^beta (construction.hpp:46-61) is emitted alongside.
 // Bounded max-heap of the KMAX smallest (d^2, original index) keys seen so far (root =
-// current worst), for the long near lists: an accepted candidate costs O(log KMAX)
-// instead of the O(KMAX) shifts of a sorted register list, which for KMAX >= 64 also
-// spills. sort() leaves the keys ascending.
-template <int KMAX>
+// current worst), kept in shared memory: element p of thread t at [p * T + t], so that
+// threads touching the same heap level hit distinct banks. An accepted candidate costs
+// O(log KMAX); the original index (tie-break key) is read only on an exact distance tie.
+// (The per-thread arrays in local memory spilled to DRAM: 35 GB per C5 build.)
+template <int KMAX, int T>
 struct NearHeap {
-    double d[KMAX];
-    uint32_t o[KMAX], j[KMAX];
+    double* d;
+    uint32_t* j;
+    const uint32_t* __restrict__ orig_of;
     int size;
-    __device__ void init() { size = 0; }
+    __device__ __forceinline__ double D(int p) const { return d[p * T]; }
+    __device__ __forceinline__ uint32_t J(int p) const { return j[p * T]; }
     __device__ __forceinline__ bool worse(int a, int b) const {  // key[a] > key[b]
-        return key_less(d[b], o[b], d[a], o[a]);
+        const double da = D(a), db = D(b);
+        return da != db ? da > db : orig_of[J(a)] > orig_of[J(b)];
     }
     __device__ __forceinline__ void swap_(int a, int b) {
-        const double td = d[a]; d[a] = d[b]; d[b] = td;
-        const uint32_t to = o[a]; o[a] = o[b]; o[b] = to;
-        const uint32_t tj = j[a]; j[a] = j[b]; j[b] = tj;
+        const double td = d[a * T]; d[a * T] = d[b * T]; d[b * T] = td;
+        const uint32_t tj = j[a * T]; j[a * T] = j[b * T]; j[b * T] = tj;
     }
     __device__ void sift_down(int p, int m) {
         for (;;) {
@@ -85,39 +88,39 @@ struct NearHeap {
             p = big;
         }
     }
-    __device__ void offer(double dd, uint32_t jj, const uint32_t* __restrict__ orig_of, int k) {
-        if (size == k && dd > d[0]) return;  // cannot enter: the original index is not read
-        const uint32_t oo = orig_of[jj];
+    __device__ void offer(double dd, uint32_t jj, int k) {
         if (size < k) {
             int p = size++;
-            d[p] = dd; o[p] = oo; j[p] = jj;
+            d[p * T] = dd; j[p * T] = jj;
             while (p > 0) {
                 const int q = (p - 1) / 2;
                 if (!worse(p, q)) break;
                 swap_(p, q);
                 p = q;
             }
-        } else if (key_less(dd, oo, d[0], o[0])) {
-            d[0] = dd; o[0] = oo; j[0] = jj;
-            sift_down(0, size);
+            return;
         }
+        const double d0 = D(0);
+        if (dd > d0 || (dd == d0 && orig_of[jj] >= orig_of[J(0)])) return;
+        d[0] = dd; j[0] = jj;
+        sift_down(0, size);
     }
     __device__ void sort() {
         for (int m = size - 1; m > 0; --m) { swap_(0, m); sift_down(0, m); }
     }
 };
 
-template <int KMAX>
+template <int KMAX, int T>
 __device__ void near_ring_search(uint32_t i, double2 q, const double2* __restrict__ xy,
-                                 const uint32_t* __restrict__ orig_of, const uint32_t* __restrict__ cell_start,
-                                 const GridParams& g, int k, NearHeap<KMAX>& t) {
-    t.init();
+                                 const uint32_t* __restrict__ cell_start, const GridParams& g, int k,
+                                 NearHeap<KMAX, T>& t) {
+    t.size = 0;
     const int32_t cx = cell_coord(q.x, g.x0, g.inv, g.gw), cy = cell_coord(q.y, g.y0, g.inv, g.gh);
     const int32_t rmax = g.gw > g.gh ? g.gw : g.gh;
     for (int32_t rho = 0; rho <= rmax; ++rho) {
         if (rho >= 1 && t.size >= k) {
             const double lb = ((double)rho - 1.0 - 1e-6) * g.cs;
-            if (lb > 0 && lb * lb > t.d[0]) break;
+            if (lb > 0 && lb * lb > t.D(0)) break;
         }
         const int32_t cnt = rho == 0 ? 1 : 8 * rho;
         for (int32_t c = 0; c < cnt; ++c) {
@@ -127,7 +130,7 @@ __device__ void near_ring_search(uint32_t i, double2 q, const double2* __restric
             const uint32_t m = morton((uint32_t)x, (uint32_t)y);
             const uint32_t s = cell_start[m], e = cell_start[m + 1];
             for (uint32_t jj = s; jj < e; ++jj)
-                if (jj != i) t.offer(dist2(q, xy[jj]), jj, orig_of, k);
+                if (jj != i) t.offer(dist2(q, xy[jj]), jj, k);
         }
     }
     t.sort();
@@ -139,18 +142,22 @@ __device__ void near_ring_search(uint32_t i, double2 q, const double2* __restric
 // candidates in uniform areas). A superblock-staged variant (3x3 superblocks in shared
 // memory, one CTA per superblock) measured 14x slower at C5: in dense clusters every
 // city scanned thousands of staged cities, and the 147 KB stage allowed one CTA per SM.
-template <int KMAX>
-__global__ void __launch_bounds__(128) k_knn_cells(const double2* __restrict__ xy, const uint32_t* __restrict__ orig_of,
-                                                   const uint32_t* __restrict__ cell_start, GridParams g, uint32_t n,
-                                                   int kk, int k, double beta, uint32_t* __restrict__ knn32,
-                                                   float* __restrict__ eta) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+template <int KMAX, int T>
+__global__ void __launch_bounds__(T) k_knn_cells(const double2* __restrict__ xy, const uint32_t* __restrict__ orig_of,
+                                                 const uint32_t* __restrict__ cell_start, GridParams g, uint32_t n,
+                                                 int kk, int k, double beta, uint32_t* __restrict__ knn32,
+                                                 float* __restrict__ eta) {
+    extern __shared__ __align__(16) unsigned char heap_smem[];  // d[KMAX][T] | j[KMAX][T]
+    const uint32_t i = blockIdx.x * T + threadIdx.x;
     if (i >= n) return;
+    NearHeap<KMAX, T> t;
+    t.d = reinterpret_cast<double*>(heap_smem) + threadIdx.x;
+    t.j = reinterpret_cast<uint32_t*>(heap_smem + sizeof(double) * KMAX * T) + threadIdx.x;
+    t.orig_of = orig_of;
     const double2 q = xy[i];
-    NearHeap<KMAX> t;
-    near_ring_search<KMAX>(i, q, xy, orig_of, cell_start, g, kk, t);
+    near_ring_search<KMAX, T>(i, q, xy, cell_start, g, kk, t);  // leaves the heap sorted
     for (int r = 0; r < KMAX; ++r) {
-        const uint32_t jj = r < kk ? t.j[r] : kNone;
+        const uint32_t jj = r < kk ? t.J(r) : kNone;
         knn32[(size_t)i * KMAX + r] = jj;
         if (r < k) {
             int32_t d = euc2d(q, xy[jj]);
