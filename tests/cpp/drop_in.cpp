@@ -41,6 +41,16 @@ int main(int argc, char** argv) {
         std::printf("drop_in ok: best %lld (%.2f%% over optimum) decisions %llu wall %.3fs\n",
                     (long long)rep.best_length, *rep.pct_error, (unsigned long long)rep.counters.decisions,
                     rep.wall_time_s);
+        // the reference's default engine: asynchronous (engine.hpp:213-244)
+        paco_b200::RunConfig acfg = cfg;
+        acfg.synchronous = false;
+        const auto arep = paco_b200::run(inst, acfg, paco_b200::Mode::partial_aco);
+        CHECK(arep.best_length >= 4420 && arep.best_tour.order.size() == 442);
+        std::int64_t alen = 0;
+        for (size_t i = 0; i < 442; ++i) alen += inst.dist(arep.best_tour.order[i], arep.best_tour.order[(i + 1) % 442]);
+        CHECK(alen == arep.best_length);
+        CHECK(arep.iterations_done == 50);
+        std::printf("drop_in async ok: best %lld\n", (long long)arep.best_length);
         // classic mode refuses n > 5000 with the reference's message (engine.hpp:158-160)
         std::vector<std::pair<double, double>> big;
         for (int i = 0; i < 5001; ++i) big.emplace_back(i % 100, i / 100);

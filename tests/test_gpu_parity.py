@@ -130,6 +130,14 @@ def test_tiny_instances(n, k):
     lockstep(inst, 6, ants=3, candidates=k, seed=n)
 
 
+@pytest.mark.parametrize("n,k", [(300, 1), (300, 2), (500, 32), (2000, 7), (1500, 15), (1500, 19)])
+def test_candidate_counts(n, k):
+    """Every scan template: k = 15/16 (KP 16), 19/20 (KP 20) and the runtime-k path (k = 1, 2,
+    7, 32), lockstep with O2 including the fallbacks."""
+    inst = make_config_instance("C1", n=n)
+    lockstep(inst, 5, ants=8, candidates=k, seed=k + 1)
+
+
 def test_duplicates_and_collinear():
     xs = np.array([5.0] * 40 + list(range(60)), dtype=float)
     ys = np.array([5.0] * 40 + [0.0] * 60, dtype=float)
