@@ -102,6 +102,13 @@ typedef struct paco_report {
     double setup_ms;           /* grid + k-NN build */
 } paco_report;
 
+/* ConvergenceSample (engine.hpp:79-83) */
+typedef struct paco_sample {
+    double elapsed_s;
+    int64_t g_best_length;
+    uint64_t iterations_done;
+} paco_sample;
+
 typedef struct paco_handle paco_handle;
 
 const char* paco_last_error(void);
@@ -150,6 +157,14 @@ paco_status paco_construct_at(paco_handle* h, uint32_t ant, uint32_t start_pos, 
  * read g_best back, destroy. best_tour may be NULL; optimum <= 0 means none. */
 paco_status paco_run(const double* xs, const double* ys, uint32_t n, const paco_config* cfg,
                      int mode, int64_t optimum, paco_report* report, uint32_t* best_tour);
+
+/* paco_run plus RunReport::convergence (engine.hpp:186-205, 327): a sample each time
+ * another cfg->convergence_interval_s of wall time has passed (taken between chunks of
+ * iterations), then the final sample. At most `cap` samples, the final one always kept;
+ * *n_samples receives the count. */
+paco_status paco_run_traced(const double* xs, const double* ys, uint32_t n, const paco_config* cfg,
+                            int mode, int64_t optimum, paco_report* report, uint32_t* best_tour,
+                            paco_sample* samples, uint32_t cap, uint32_t* n_samples);
 
 #ifdef __cplusplus
 }

@@ -163,8 +163,10 @@ inline RunReport run(const Instance& inst, const RunConfig& cfg, Mode mode) {
     paco_report rep{};
     RunReport out;
     out.best_tour.order.resize(inst.n());
-    check(paco_run(inst.xs(), inst.ys(), inst.n(), &c, to_c(mode), inst.optimum().value_or(0), &rep,
-                   out.best_tour.order.data()));
+    std::vector<paco_sample> samples(4096);
+    std::uint32_t ns = 0;
+    check(paco_run_traced(inst.xs(), inst.ys(), inst.n(), &c, to_c(mode), inst.optimum().value_or(0), &rep,
+                          out.best_tour.order.data(), samples.data(), (std::uint32_t)samples.size(), &ns));
     out.best_length = rep.best_length;
     out.best_tour.length = rep.best_length;
     if (inst.optimum()) out.pct_error = rep.pct_error;
@@ -175,7 +177,8 @@ inline RunReport run(const Instance& inst, const RunConfig& cfg, Mode mode) {
     out.construct_ms = rep.construct_ms;
     out.update_ms = rep.update_ms;
     out.setup_ms = rep.setup_ms;
-    out.convergence.push_back({out.wall_time_s, out.best_length, out.iterations_done});
+    for (std::uint32_t i = 0; i < ns; ++i)
+        out.convergence.push_back({samples[i].elapsed_s, samples[i].g_best_length, samples[i].iterations_done});
     return out;
 }
 

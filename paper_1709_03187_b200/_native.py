@@ -29,7 +29,7 @@ EXPORTED = (
     "paco_last_error", "paco_version", "paco_config_default", "paco_config_validate", "paco_create",
     "paco_destroy", "paco_iterate", "paco_set_draws", "paco_get_tours", "paco_get_l_best",
     "paco_get_g_best", "paco_get_counters", "paco_get_build_flags", "paco_get_candidates",
-    "paco_get_timing", "paco_offer_tour", "paco_construct_at", "paco_run",
+    "paco_get_timing", "paco_offer_tour", "paco_construct_at", "paco_run", "paco_run_traced",
 )
 
 
@@ -51,6 +51,10 @@ class Counters(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+class Sample(ctypes.Structure):
+    _fields_ = [("elapsed_s", c_double), ("g_best_length", c_int64), ("iterations_done", c_uint64)]
 
 
 class Report(ctypes.Structure):
@@ -109,6 +113,8 @@ def load() -> ctypes.CDLL:
                                       P(c_int64)]),
         "paco_run": (c_int, [P(c_double), P(c_double), c_uint32, P(Config), c_int, c_int64, P(Report),
                              P(c_uint32)]),
+        "paco_run_traced": (c_int, [P(c_double), P(c_double), c_uint32, P(Config), c_int, c_int64, P(Report),
+                                    P(c_uint32), P(Sample), c_uint32, P(c_uint32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -843,10 +843,12 @@ paco_status paco_construct_at(paco_handle* h, uint32_t ant, uint32_t start_pos, 
     return PACO_OK;
 }
 
-paco_status paco_run(const double* xs, const double* ys, uint32_t n, const paco_config* cfg, int mode,
-                     int64_t optimum, paco_report* rep, uint32_t* best_tour) {
+paco_status paco_run_traced(const double* xs, const double* ys, uint32_t n, const paco_config* cfg, int mode,
+                            int64_t optimum, paco_report* rep, uint32_t* best_tour, paco_sample* samples,
+                            uint32_t cap, uint32_t* n_samples) {
     if (!rep) return fail(PACO_E_INVALID, "null report");
     if (cfg && cfg->draws == PACO_DRAWS_BUFFER) return fail(PACO_E_INVALID, "paco_run uses Philox draws");
+    if (n_samples) *n_samples = 0;
     const auto t0 = std::chrono::steady_clock::now();
     auto since = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     paco_handle* h = nullptr;
@@ -854,19 +856,35 @@ paco_status paco_run(const double* xs, const double* ys, uint32_t n, const paco_
     if (s != PACO_OK) return s;
     double c_ms = 0, u_ms = 0;
     uint64_t done = 0;
-    if (cfg->time_budget_s <= 0.0) {
-        s = paco_iterate(h, cfg->iterations);
-        c_ms = h->construct_ms; u_ms = h->update_ms;
-        done = cfg->iterations;
-    } else {
-        // engine.hpp:270-272: the in-flight iteration always completes
-        while (done < cfg->iterations && s == PACO_OK) {
-            s = paco_iterate(h, 1);
-            c_ms += h->construct_ms; u_ms += h->update_ms;
-            ++done;
-            if (since() >= cfg->time_budget_s) break;
+    // Convergence monitor (engine.hpp:186-205): a sample of (elapsed, g_best, iterations)
+    // each time another convergence_interval_s of wall time has passed, taken between
+    // chunks of iterations sized from the measured iteration time. Synchronous results do
+    // not depend on the chunking; the last slot is kept for the final sample.
+    const double interval = cfg->convergence_interval_s;
+    const bool sampling = interval > 0.0 && samples && cap > 1;
+    uint32_t ns = 0;
+    double next_t = interval;
+    const bool budgeted = cfg->time_budget_s > 0.0;
+    uint64_t chunk = (sampling || budgeted) ? 1 : cfg->iterations;
+    while (done < cfg->iterations && s == PACO_OK) {
+        const uint64_t c = std::min<uint64_t>(chunk, cfg->iterations - done);
+        s = paco_iterate(h, c);
+        c_ms += h->construct_ms; u_ms += h->update_ms;
+        done += c;
+        const double t = since();
+        if (s == PACO_OK && sampling && t >= next_t && ns + 1 < cap) {
+            GBest g{};
+            if (cudaMemcpy(&g, h->gb, sizeof g, cudaMemcpyDeviceToHost) == cudaSuccess && g.has)
+                samples[ns++] = paco_sample{t, g.len, done};
+            while (next_t <= t) next_t += interval;
+        }
+        if (budgeted && t >= cfg->time_budget_s) break;  // engine.hpp:270-272: the in-flight iteration completes
+        if (sampling && !budgeted) {
+            const double per_iter = t / (double)done;
+            chunk = (uint64_t)std::max(1.0, std::floor((next_t - t) / std::max(per_iter, 1e-9)));
         }
     }
+    if (s == PACO_OK && n_samples) *n_samples = ns;
     if (s != PACO_OK) { paco_destroy(h); return s; }
     std::vector<uint32_t> tour(n);
     int64_t len = 0;
@@ -885,7 +903,16 @@ paco_status paco_run(const double* xs, const double* ys, uint32_t n, const paco_
     rep->construct_ms = c_ms; rep->update_ms = u_ms;
     if (best_tour) std::memcpy(best_tour, tour.data(), sizeof(uint32_t) * n);
     rep->wall_time_s = since();
+    if (samples && cap > 0 && n_samples) {  // engine.hpp:327: the final sample
+        samples[ns] = paco_sample{rep->wall_time_s, len, done};
+        *n_samples = ns + 1;
+    }
     return PACO_OK;
+}
+
+paco_status paco_run(const double* xs, const double* ys, uint32_t n, const paco_config* cfg, int mode,
+                     int64_t optimum, paco_report* rep, uint32_t* best_tour) {
+    return paco_run_traced(xs, ys, n, cfg, mode, optimum, rep, best_tour, nullptr, 0, nullptr);
 }
 
 } // extern "C"

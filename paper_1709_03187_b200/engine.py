@@ -224,14 +224,18 @@ def run(inst: Instance, cfg: RunConfig, mode: Mode = Mode.partial_aco) -> RunRep
     rep = N.Report()
     best = np.empty(inst.n, np.uint32)
     opt = inst.optimum if inst.optimum else 0
-    N.check(lib.paco_run(_dptr(inst.xs), _dptr(inst.ys), inst.n, ctypes.byref(cfg.to_c()), int(mode), opt,
-                         ctypes.byref(rep), _u32(best)))
+    cap = 4096
+    samples = (N.Sample * cap)()
+    ns = ctypes.c_uint32()
+    N.check(lib.paco_run_traced(_dptr(inst.xs), _dptr(inst.ys), inst.n, ctypes.byref(cfg.to_c()), int(mode), opt,
+                                ctypes.byref(rep), _u32(best), samples, cap, ctypes.byref(ns)))
     out = RunReport(best_length=int(rep.best_length), best_tour=Tour(best, int(rep.best_length)),
                     pct_error=None if math.isnan(rep.pct_error) else float(rep.pct_error),
                     wall_time_s=float(rep.wall_time_s), iterations_done=int(rep.iterations_done),
                     comparisons_total=int(rep.comparisons_total), counters=rep.counters.as_dict(),
                     construct_ms=rep.construct_ms, update_ms=rep.update_ms, setup_ms=rep.setup_ms)
-    out.convergence.append(ConvergenceSample(out.wall_time_s, out.best_length, out.iterations_done))
+    out.convergence = [ConvergenceSample(float(x.elapsed_s), int(x.g_best_length), int(x.iterations_done))
+                       for x in samples[:ns.value]]
     return out
 
 

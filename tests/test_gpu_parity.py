@@ -212,6 +212,25 @@ def test_large_configs_properties(cfg_name):
             g_prev = g
 
 
+def test_convergence_trace():
+    """RunReport::convergence (engine.hpp:186-205, 327): samples while running plus the final
+    one; synchronous results do not depend on the sampling."""
+    inst = make_config_instance("C2", n=6000)
+    base = RunConfig(ants=64, iterations=40, alpha=1.0, beta=2.0, candidates=16, seed=2, convergence_interval_s=0.0)
+    plain = run(inst, base)
+    from dataclasses import replace
+    traced = run(inst, replace(base, convergence_interval_s=0.002))
+    assert traced.best_length == plain.best_length
+    assert np.array_equal(traced.best_tour.order, plain.best_tour.order)
+    conv = traced.convergence
+    assert len(conv) >= 3
+    assert all(a.elapsed_s < b.elapsed_s for a, b in zip(conv, conv[1:]))
+    assert all(a.g_best_length >= b.g_best_length for a, b in zip(conv, conv[1:]))
+    assert all(a.iterations_done < b.iterations_done for a, b in zip(conv[:-1], conv[1:-1]))
+    assert conv[-1].g_best_length == traced.best_length and conv[-1].iterations_done == 40
+    assert len(plain.convergence) == 1
+
+
 def test_run_api_matches_colony():
     inst = make_config_instance("C1", n=500)
     cfg = RunConfig(ants=16, iterations=12, alpha=1.0, beta=2.0, candidates=20, seed=5)
