@@ -936,25 +936,54 @@ __global__ void k_gbest_from_gkey(const unsigned long long* __restrict__ gkey, G
 // colony.hpp:117-124) then update_g_best (colony.hpp:127-139). The l_best switch is
 // a flip of the ant's double-buffer selector, so no tour is copied.
 
-__global__ void k_update(uint32_t first, uint32_t count, const int64_t* __restrict__ new_len,
-                         int64_t* __restrict__ lb_len, uint8_t* __restrict__ has_lb, uint8_t* __restrict__ lb_sel,
-                         uint8_t* __restrict__ improved, GBest* __restrict__ gb, int64_t* __restrict__ g_len,
-                         unsigned long long* __restrict__ counters) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    GBest g = *gb;
-    unsigned long long imp = 0;
-    for (uint32_t a = first; a < first + count; ++a) {
+// The ants' l_best updates are independent; the g_best update sequence in ant order with
+// strict improvement ends at the lexicographic minimum (length, ant) of the improved ants
+// when that beats the incumbent, so it is one block-wide argmin. One CTA.
+__global__ void __launch_bounds__(1024) k_update(uint32_t first, uint32_t count, const int64_t* __restrict__ new_len,
+                                                 int64_t* __restrict__ lb_len, uint8_t* __restrict__ has_lb,
+                                                 uint8_t* __restrict__ lb_sel, uint8_t* __restrict__ improved,
+                                                 GBest* __restrict__ gb, int64_t* __restrict__ g_len,
+                                                 unsigned long long* __restrict__ counters) {
+    __shared__ long long s_len[32];
+    __shared__ int32_t s_ant[32];
+    __shared__ unsigned s_imp[32];
+    long long bl = 0x7fffffffffffffffLL;
+    int32_t ba = -1;
+    unsigned imp = 0;
+    for (uint32_t a = first + threadIdx.x; a < first + count; a += blockDim.x) {
         const int64_t L = new_len[a];
         if (!has_lb[a] || L < lb_len[a]) {
             has_lb[a] = 1; lb_len[a] = L; lb_sel[a] ^= 1; improved[a] = 1; ++imp;
-            if (!g.has || L < g.len) { g.len = L; g.ant = (int32_t)a; g.has = 1; }
+            if (L < bl) { bl = L; ba = (int32_t)a; }  // ants visited in increasing order per thread
         } else {
             improved[a] = 0;
         }
     }
-    *gb = g;
-    *g_len = g.has ? g.len : 0x7fffffffffffffffLL;
-    counters[7] += imp;
+    auto better = [](long long l1, int32_t a1, long long l2, int32_t a2) {
+        return a1 >= 0 && (a2 < 0 || l1 < l2 || (l1 == l2 && a1 < a2));
+    };
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const long long l2 = __shfl_xor_sync(kFull, bl, off);
+        const int32_t a2 = __shfl_xor_sync(kFull, ba, off);
+        imp += __shfl_xor_sync(kFull, imp, off);
+        if (better(l2, a2, bl, ba)) { bl = l2; ba = a2; }
+    }
+    const uint32_t w = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) { s_len[w] = bl; s_ant[w] = ba; s_imp[w] = imp; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (uint32_t q = 0; q < nwarps; ++q) {
+            tot += s_imp[q];
+            if (better(s_len[q], s_ant[q], bl, ba)) { bl = s_len[q]; ba = s_ant[q]; }
+        }
+        GBest g = *gb;
+        if (ba >= 0 && (!g.has || bl < g.len)) { g.len = bl; g.ant = ba; g.has = 1; }
+        *gb = g;
+        *g_len = g.has ? g.len : 0x7fffffffffffffffLL;
+        counters[7] += tot;
+    }
 }
 
 // Ant::publish (colony.hpp:39-52) for the improved ants: neighbour pairs of the new

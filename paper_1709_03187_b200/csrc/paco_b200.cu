@@ -604,7 +604,7 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
             else k_classic<32><<<nb, 256, 0, h->st>>>(h->knn, h->cur_nbr, h->new_len, n, m, (int)h->k, h->cfg.rho, h->T);
             CU(cudaGetLastError());
         }
-        k_update<<<1, 32, 0, h->st>>>(0, m, h->new_len, h->lb_len, h->has_lb, h->lb_sel, h->improved, h->gb,
+        k_update<<<1, std::min<uint32_t>(1024, (m + 31) & ~31u), 0, h->st>>>(0, m, h->new_len, h->lb_len, h->has_lb, h->lb_sel, h->improved, h->gb,
                                       h->g_len, h->counters);
         dim3 grid((n + 255) / 256, m);
         k_publish<<<grid, 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, n, 0, h->nbr);
