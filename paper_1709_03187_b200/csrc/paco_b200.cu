@@ -1,9 +1,12 @@
 // Host side of the B200 tour-construction engine and its C ABI (include/paco_b200.h).
-// One handle = one instance + one colony resident in HBM + one CUDA stream.
-// An iteration is five launches on that stream:
+// One handle = one instance + one colony resident in HBM + one CUDA stream (two in
+// asynchronous mode). A synchronous iteration is these launches on that stream
+// (DESIGN.md §4):
 //   K5 k_weights  -> K2 k_construct -> [K6 classic deposit] -> K4 k_update -> k_publish
 // which together replace one barrier-synchronous iteration of paco::run
-// (/root/reference/proj/include/paco/engine.hpp:245-306).
+// (/root/reference/proj/include/paco/engine.hpp:245-306). Asynchronous calls
+// (engine.hpp:213-244) are one k_construct_async launch with k_weights passes running
+// beside it on the second stream.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -482,8 +485,7 @@ static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint
     auto launch = [&](auto kern) -> paco_status {
         if (smem > 48 * 1024)
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        if (getenv("PACO_CARVEOUT")) CU(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(getenv("PACO_CARVEOUT"))));
-        else CU(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         kern<<<blocks, 32, smem, h->st>>>(a);
         CU(cudaGetLastError());
         return PACO_OK;
