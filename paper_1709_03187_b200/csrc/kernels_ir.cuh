@@ -5,8 +5,8 @@
 // same lengths, same g_best, same comparison count.
 //
 // This mode exists for parity, not speed: the rule scans O(n) candidates per decision
-// and the streams are sequential, so lane 0 generates the draws of each 32-city chunk
-// while the warp scores them. Cities are kept in their original order (identity
+// and the streams are sequential, so a generator warp runs each ant's stream ahead while
+// the construction warp scores. Cities are kept in their original order (identity
 // internal numbering) because the rule consumes draws in ascending city index.
 #pragma once
 #include "device.cuh"
@@ -57,48 +57,98 @@ struct IrArgs {
     uint32_t two_opt_window;
 };
 
-// One warp per ant: detail::build_candidate (engine.hpp:129-148) with construct_full /
-// construct_partial (construction.hpp:283-365) and select_next (construction.hpp:246-281).
-__global__ void __launch_bounds__(32, 1) k_construct_ir(IrArgs a) {
+// Draw ring between the generator warp and the construction warp of one ant.
+constexpr uint32_t kIrRing = 2048;          // u64 draws in flight
+constexpr uint32_t kIrCkpt = kIrRing / 32;  // generator states saved every 32 draws
+struct IrRing {
+    unsigned long long draw[kIrRing];
+    unsigned long long ckpt[kIrCkpt][4];    // state before draw 32c (slot c % kIrCkpt)
+    double stage[32];                       // begin_step contributions of one pass
+    volatile uint32_t produced, consumed, stop;
+};
+
+// One CTA of two warps per ant: detail::build_candidate (engine.hpp:129-148) with
+// construct_full / construct_partial (construction.hpp:283-365) and select_next
+// (construction.hpp:246-281).
+//  * warp 1, lane 0 runs the ant's xoshiro256++ stream ahead into a shared-memory ring;
+//  * warp 0 builds the tour, consuming the draws in the reference's order.
+// The stream is inherently sequential; with the generator on its own warp it overlaps
+// the scoring instead of alternating with it. The draws a construction actually consumed
+// decide the stored stream state: the generator checkpoints its state every 32 draws
+// and never runs so far ahead that the checkpoint below the consumption point is
+// overwritten; the construction warp replays at most 31 steps from it.
+__global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const uint32_t lane = threadIdx.x, ant = blockIdx.x, n = a.n, nw = a.nwords;
-    double* acc = reinterpret_cast<double*>(smem_raw);              // n (P-ACO): ColonyPheromone::acc_
-    uint64_t* dbuf = reinterpret_cast<uint64_t*>(acc + (a.T ? 0 : n)); // 32 draws of the current chunk
-    uint32_t* vis = reinterpret_cast<uint32_t*>(dbuf + 32);          // nw
-    uint64_t s[4] = {0, 0, 0, 0};  // lane 0 owns the stream
-    if (lane == 0)
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, ant = blockIdx.x, n = a.n, nw = a.nwords;
+    IrRing* ring = reinterpret_cast<IrRing*>(smem_raw);
+    double* acc = reinterpret_cast<double*>(ring + 1);                 // n (P-ACO): ColonyPheromone::acc_
+    uint32_t* vis = reinterpret_cast<uint32_t*>(acc + (a.T ? 0 : n));  // nw
+    if (threadIdx.x == 0) { ring->produced = 0; ring->consumed = 0; ring->stop = 0; }
+    if (warp == 0) {
+        if (!a.T)
+            for (uint32_t j = lane; j < n; j += 32) acc[j] = 0.0;
+        for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
+    }
+    __syncthreads();
+    if (warp == 1) {
+        if (lane != 0) return;
+        // the generator (rng.hpp:40-50), state carried across iterations in a.rng
+        uint64_t s[4];
         for (int q = 0; q < 4; ++q) s[q] = a.rng[(size_t)ant * 4 + q];
-    if (!a.T)
-        for (uint32_t j = lane; j < n; j += 32) acc[j] = 0.0;
-    for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
-    __syncwarp();
+        uint32_t p = 0;
+        for (;;) {
+            if ((p & 31u) == 0) {
+                if (p - ring->consumed >= kIrRing - 32) {  // keep the consumption checkpoint alive
+                    __threadfence_block();
+                    ring->produced = p;
+                    while (p - ring->consumed >= kIrRing - 32 && !ring->stop) __nanosleep(200);
+                }
+                if (ring->stop) return;
+                unsigned long long* c = ring->ckpt[(p >> 5) % kIrCkpt];
+                c[0] = s[0]; c[1] = s[1]; c[2] = s[2]; c[3] = s[3];
+            }
+            ring->draw[p % kIrRing] = xoshiro_next(s);
+            ++p;
+            if ((p & 31u) == 0) { __threadfence_block(); ring->produced = p; }
+        }
+    }
+    // ---- warp 0: the construction ----
     if (lane == 0 && (n & 31)) vis[nw - 1] = 0xffffffffu << (n & 31);
     __syncwarp();
+    uint32_t cidx = 0;  // draws consumed so far (warp-uniform)
+    auto wait_for = [&](uint32_t upto) {  // draws [0, upto) are in the ring
+        if (lane == 0) while (ring->produced < upto) {}
+        __syncwarp();
+        __threadfence_block();
+    };
+    auto take = [&]() -> uint64_t {  // next draw, lane 0's view (other lanes follow the index)
+        wait_for(cidx + 1);
+        const uint64_t v = ring->draw[cidx % kIrRing];
+        ++cidx;
+        return v;
+    };
+    auto uniform = [&]() { return (double)(take() >> 11) * 0x1.0p-53; };  // Rng::uniform, rng.hpp:53-55
+    auto below = [&](uint32_t bound) {  // Rng::uniform_below, rng.hpp:59-66
+        const uint32_t mask = bound <= 1 ? 0u : (0xffffffffu >> __clz(bound - 1));
+        for (;;) {
+            const uint32_t r = (uint32_t)take() & mask;
+            if (r < bound) return r;
+        }
+    };
     const uint8_t sel = a.lb_sel[ant];
     uint32_t* out = a.tours + ((size_t)ant * 2 + (1 - sel)) * n;
     const uint32_t* lb = a.tours + ((size_t)ant * 2 + sel) * n;
 
-    // lane-0 draws broadcast to the warp
-    auto bcast = [&](uint32_t v) { return __shfl_sync(kFull, v, 0); };
     int partial = 0;
     uint32_t start_pos = 0, m_mod = 0, start = 0;
-    {
-        uint32_t p = 0, sp = 0, mm = 0, st = 0;
-        if (lane == 0) {
-            if (!a.seeding || a.coin_always) {
-                const double coin = xo_uniform(s);  // engine.hpp:137
-                p = coin < a.eff_pp ? 1 : 0;
-            }
-            if (p) {
-                sp = xo_below(s, n);  // construction.hpp:358
-                double capd = floor(a.mmf * (double)n);
-                if (capd < 2.0) capd = 2.0;
-                mm = 2 + xo_below(s, (uint32_t)capd - 1);
-            } else {
-                st = xo_below(s, n);  // construction.hpp:291
-            }
-        }
-        partial = (int)bcast(p); start_pos = bcast(sp); m_mod = bcast(mm); start = bcast(st);
+    if (!a.seeding || a.coin_always) partial = uniform() < a.eff_pp ? 1 : 0;  // engine.hpp:137
+    if (partial) {
+        start_pos = below(n);  // construction.hpp:358
+        double capd = floor(a.mmf * (double)n);
+        if (capd < 2.0) capd = 2.0;
+        m_mod = 2 + below((uint32_t)capd - 1);
+    } else {
+        start = below(n);  // construction.hpp:291
     }
     uint32_t pos, cur, remaining;
     if (!partial) {
@@ -126,8 +176,9 @@ __global__ void __launch_bounds__(32, 1) k_construct_ir(IrArgs a) {
     __syncwarp();
 
     unsigned long long n_dec = 0, n_cmp = 0, n_forced = 0;
+    // untouched cities score with tau0^alpha (ColonyPheromone::mult_, construction.hpp:108-111);
+    // a touched city always has acc > 0 (contributions are g/l ratios > 0)
     const double tau0_alpha = power(a.alpha, a.tau0);
-    (void)tau0_alpha;
     // full constructions score every step (the last one with a single candidate);
     // partial constructions append the final city unscored (construction.hpp:338-348)
     const uint32_t scored = partial ? (remaining > 0 ? remaining - 1 : 0) : remaining;
@@ -148,17 +199,30 @@ __global__ void __launch_bounds__(32, 1) k_construct_ir(IrArgs a) {
             }
             ++n_forced;
         } else {
-            // ColonyPheromone::begin_step (construction.hpp:121-132): ant order, lane 0
+            // ColonyPheromone::begin_step (construction.hpp:121-132): the 2m contributions
+            // (ant q's prev then next of cur) in order, 32 per pass, one lane each. Lanes
+            // that hit the same city are grouped (match.any) and the group's lowest lane
+            // adds them in lane order, so every acc[c] receives its terms in ant order -
+            // the fp64 sum order of the reference.
             if (!a.T) {
-                if (lane == 0)
-                    for (uint32_t q = 0; q < a.m; ++q) {
-                        const double r = a.ratio[q];
-                        if (r == 0.0) continue;
+                for (uint32_t e0 = 0; e0 < 2 * a.m; e0 += 32) {
+                    const uint32_t e = e0 + lane, q = e >> 1;
+                    const double r = e < 2 * a.m ? a.ratio[q] : 0.0;
+                    uint32_t c = kNone;
+                    if (r != 0.0) {
                         const uint2 pr = a.nbr[(size_t)q * n + cur];
-                        acc[pr.x] += r;
-                        acc[pr.y] += r;
+                        c = (e & 1u) ? pr.y : pr.x;
                     }
-                __syncwarp();
+                    ring->stage[lane] = r;
+                    const unsigned grp = __match_any_sync(kFull, c);
+                    __syncwarp();
+                    if (c != kNone && (int)lane == __ffs(grp) - 1) {
+                        double v = acc[c];
+                        for (unsigned g = grp; g; g &= g - 1) v += ring->stage[__ffs(g) - 1];
+                        acc[c] = v;
+                    }
+                    __syncwarp();
+                }
             }
             const double2 qc = a.xy[cur];
             const double* trow = a.T ? a.T + (size_t)cur * n : nullptr;
@@ -170,21 +234,26 @@ __global__ void __launch_bounds__(32, 1) k_construct_ir(IrArgs a) {
                 if (!free_bits) continue;
                 const uint32_t cnt = __popc(free_bits);
                 cnt_total += cnt;
-                if (lane == 0)
-                    for (uint32_t q = 0; q < cnt; ++q) dbuf[q] = xoshiro_next(s);  // one draw per candidate
-                __syncwarp();
+                wait_for(cidx + cnt);  // one draw per candidate, ascending city index
                 if ((free_bits >> lane) & 1u) {
                     const uint32_t j = w * 32 + lane;
-                    const double u = (double)(dbuf[__popc(free_bits & ((1u << lane) - 1u))] >> 11) * 0x1.0p-53;
+                    const uint64_t raw = ring->draw[(cidx + __popc(free_bits & ((1u << lane) - 1u))) % kIrRing];
+                    const double u = (double)(raw >> 11) * 0x1.0p-53;
                     int32_t d = euc2d(qc, a.xy[j]);
                     if (d < 1) d = 1;
                     double eta = power(a.beta, 1.0 / (double)d);
                     if (a.eta_table) eta = (double)(float)eta;
-                    const double ta = trow ? power(a.alpha, trow[j]) : power(a.alpha, __dadd_rn(a.tau0, acc[j]));
+                    double ta;
+                    if (trow) ta = power(a.alpha, trow[j]);
+                    else {
+                        const double aj = acc[j];
+                        ta = aj == 0.0 ? tau0_alpha : power(a.alpha, __dadd_rn(a.tau0, aj));
+                    }
                     const double score = __dmul_rn(__dmul_rn(ta, eta), u);
                     if (score > best) { best = score; bj = j; }
                 }
-                __syncwarp();
+                cidx += cnt;
+                if (lane == 0) ring->consumed = cidx;
             }
             // warp argmax, strict >, lowest city index on equal scores
 #pragma unroll
@@ -213,9 +282,17 @@ __global__ void __launch_bounds__(32, 1) k_construct_ir(IrArgs a) {
         cur = next;
     }
     // maybe_two_opt consumes exactly one draw (two_opt.hpp:71-76)
-    uint32_t do2 = 0;
-    if (lane == 0) do2 = xo_uniform(s) < a.two_opt_prob ? 1u : 0u;
-    do2 = __shfl_sync(kFull, do2, 0);
+    const uint32_t do2 = uniform() < a.two_opt_prob ? 1u : 0u;
+    // stop the generator; the stream state after exactly cidx draws: the checkpoint at
+    // cidx rounded down to 32 (still alive, see above) advanced by the remainder
+    if (lane == 0) {
+        ring->consumed = cidx;
+        ring->stop = 1;
+        const unsigned long long* c = ring->ckpt[(cidx >> 5) % kIrCkpt];
+        uint64_t s[4] = {c[0], c[1], c[2], c[3]};
+        for (uint32_t q = 0; q < (cidx & 31u); ++q) xoshiro_next(s);
+        for (int q = 0; q < 4; ++q) a.rng[(size_t)ant * 4 + q] = s[q];
+    }
     __syncwarp();
     if (do2) two_opt_warp(out, n, a.two_opt_window, a.xy, lane);
     long long len = 0;
@@ -223,7 +300,6 @@ __global__ void __launch_bounds__(32, 1) k_construct_ir(IrArgs a) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) len += __shfl_xor_sync(kFull, len, off);
     if (lane == 0) {
-        for (int q = 0; q < 4; ++q) a.rng[(size_t)ant * 4 + q] = s[q];
         a.new_len[ant] = len;
         a.partial_flag[ant] = (uint8_t)partial;
         atomicAdd(&a.counters[0], n_dec);

@@ -187,9 +187,9 @@ static paco_status build_grid(paco_handle* h) {
     return PACO_OK;
 }
 
-// reference rule: [acc n doubles (P-ACO)] [32 draws] [bitmap]
+// reference rule: [draw ring] [acc n doubles (P-ACO)] [bitmap]
 static size_t ir_smem_bytes(uint32_t n, uint32_t nwords, int mode) {
-    return (mode == PACO_MODE_CLASSIC ? 0 : (size_t)8 * n) + 32 * 8 + (size_t)nwords * 4;
+    return sizeof(IrRing) + (mode == PACO_MODE_CLASSIC ? 0 : (size_t)8 * n) + (size_t)nwords * 4;
 }
 
 // colony state shared by both selection rules
@@ -452,7 +452,7 @@ static paco_status launch_construct_ir(paco_handle* h, bool seeding) {
     const size_t smem = ir_smem_bytes(h->n, h->nwords, h->mode);
     if (smem > 48 * 1024)
         CU(cudaFuncSetAttribute(k_construct_ir, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_construct_ir<<<h->m, 32, smem, h->st>>>(a);
+    k_construct_ir<<<h->m, 64, smem, h->st>>>(a);
     CU(cudaGetLastError());
     return PACO_OK;
 }
