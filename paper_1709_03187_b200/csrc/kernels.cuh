@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(T) k_knn_cells(const double2* __restrict__ xy,
 // Classic mode reads tau from the candidate-edge pheromone table T instead.
 // Output: packed {c_r, w} rows, the only table the construction kernel reads.
 template <int KMAX, bool LIVE>
-__global__ void __launch_bounds__(256) k_weights(const uint32_t* __restrict__ knn32, const float* __restrict__ eta,
+__global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__ knn32, const float* __restrict__ eta,
                                                  const uint2* __restrict__ nbr, const int64_t* __restrict__ lb_len,
                                                  const uint8_t* __restrict__ has_lb, const int64_t* __restrict__ g_len,
                                                  const unsigned long long* __restrict__ gkey,
