@@ -344,6 +344,14 @@ __device__ __forceinline__ void warp_argmin_redux(double& d, uint32_t& o, uint32
     d = __longlong_as_double((long long)(((unsigned long long)hmin << 32) | lmin));
 }
 
+#ifdef PACO_SEG
+__device__ __forceinline__ long long seg_clk(uint32_t dep) {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c) : "r"(dep) : "memory");
+    return c;
+}
+#endif
+
 #ifdef PACO_FB_INLINE
 #define PACO_FB_ATTR __forceinline__
 #else
@@ -659,6 +667,9 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
 #endif
     // candidate row entry of the current decision
     const uint32_t n_free = n_dec > 0 ? n_dec - 1 : 0;  // roulette / fallback decisions
+#ifdef PACO_SEG
+    long long sq_tail = 0, sq_probe = 0, sq_scan = 0, sq_pick = 0, sq_n = 0, sq_prev = clock64();
+#endif
     uint2 e_pre = ldg_u64_if(row_base + (size_t)cur * kp, lane_in && n_free > 0, make_uint2(cur, 0u));
     // Decisions in batches of 128: each lane holds the Philox block of 4 decisions of the
     // batch (draw slot 4 + t), handed out by shuffle. Inside a batch the only branch is
@@ -673,12 +684,18 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         for (uint32_t t = t0; t < t1; ++t) {
             __syncwarp();  // orders the previous decision's visited-bit update for every lane
             const uint2 e = e_pre;  // requested at the end of the previous decision
+#ifdef PACO_SEG
+            const long long sg0 = seg_clk(e.x);
+#endif
             // feasibility from the bitmap
             const uint32_t vw_addr = vis_s + ((e.x >> 5) << 2);
             const uint32_t vw = lds_u32(vw_addr);
             const uint32_t uw = BUF ? wrow[4 + t] : __shfl_sync(kFull, pick_word(pb, t & 3), (t & 127) >> 2);
             const uint32_t bit = 1u << (e.x & 31);
             const float w = (vw & bit) ? 0.0f : __uint_as_float(e.y);
+#ifdef PACO_SEG
+            const long long sg1 = seg_clk(__float_as_uint(w));
+#endif
             // Pull every feasible candidate's row into L1 with predicated cp.async.ca (one
             // 16-byte copy per 32-byte sector into a per-lane scratch slot that is never
             // read): the winner's row is then an L1 hit for the next decision.
@@ -710,6 +727,9 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
                 if (lane >= (1u << st)) v = __fadd_rn(v, y);
             }
             const float S = __shfl_sync(kFull, v, k - 1);
+#ifdef PACO_SEG
+            const long long sg2 = seg_clk(__float_as_uint(S));
+#endif
             uint32_t next;
             if (feas) {
                 const float u = u01_f32(uw);
@@ -731,12 +751,20 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
                 // decision's probe does not depend on it.
                 sts_u32_if(vw_addr, vw | bit, lane == r);
                 n_tie += tie ? 1u : 0u;
+#ifdef PACO_SEG
+                const long long sg3 = seg_clk(next);
+                sq_tail += sg0 - sq_prev; sq_probe += sg1 - sg0; sq_scan += sg2 - sg1; sq_pick += sg3 - sg2; ++sq_n;
+                sq_prev = sg3;
+#endif
             } else {
 #ifdef PACO_TIMING
                 const long long c0 = clock64();
 #endif
                 next = nearest_unvisited(fctx, vis_s, cur, lane, fb_s, fs);
                 if (lane == 0) vis[next >> 5] |= 1u << (next & 31);
+#ifdef PACO_SEG
+                sq_prev = seg_clk(next);
+#endif
 #ifdef PACO_TIMING
                 fbc += clock64() - c0;
 #endif
@@ -767,6 +795,13 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         ++pos;
     }
     const uint32_t n_forced = n_dec > 0 ? 1u : 0u;
+#ifdef PACO_SEG
+    if (lane == 0 && sq_n > 1) {
+        atomicAdd(&g_timing[4], (unsigned long long)sq_tail); atomicAdd(&g_timing[5], (unsigned long long)sq_probe);
+        atomicAdd(&g_timing[6], (unsigned long long)sq_scan); atomicAdd(&g_timing[7], (unsigned long long)sq_pick);
+        atomicAdd(&g_timing[8], (unsigned long long)sq_n);
+    }
+#endif
     cp_async_wait_all();
     __syncwarp();
 #ifdef PACO_TIMING
