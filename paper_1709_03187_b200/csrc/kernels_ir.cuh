@@ -44,6 +44,7 @@ struct IrArgs {
     const uint2* nbr;         // m*n (prev, next) of each ant's l_best (P-ACO)
     const double* ratio;      // m g/l ratios snapshotted for this iteration (0 = no tour)
     const double* T;          // classic: n*n pheromone matrix, else nullptr
+    const float* eta_tab;     // n*n eta^beta as f32 (the reference's table path, n <= 5000), else nullptr
     uint64_t* rng;            // m*4 xoshiro256++ states, carried across iterations
     uint32_t* tours;          // m*2*n
     const uint8_t* lb_sel;
@@ -57,13 +58,22 @@ struct IrArgs {
     uint32_t two_opt_window;
 };
 
+// acquire / release on shared-memory flags (no full fence between the two warps)
+__device__ __forceinline__ uint32_t ld_acquire_cta(const volatile uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared((const void*)p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(volatile uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared((const void*)p)), "r"(v) : "memory");
+}
+
 // Draw ring between the generator warp and the construction warp of one ant.
 constexpr uint32_t kIrRing = 2048;          // u64 draws in flight
 constexpr uint32_t kIrCkpt = kIrRing / 32;  // generator states saved every 32 draws
 struct IrRing {
     unsigned long long draw[kIrRing];
     unsigned long long ckpt[kIrCkpt][4];    // state before draw 32c (slot c % kIrCkpt)
-    double stage[32];                       // begin_step contributions of one pass
     volatile uint32_t produced, consumed, stop;
 };
 
@@ -82,7 +92,9 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, ant = blockIdx.x, n = a.n, nw = a.nwords;
     IrRing* ring = reinterpret_cast<IrRing*>(smem_raw);
     double* acc = reinterpret_cast<double*>(ring + 1);                 // n (P-ACO): ColonyPheromone::acc_
-    uint32_t* vis = reinterpret_cast<uint32_t*>(acc + (a.T ? 0 : n));  // nw
+    double* stage_r = acc + (a.T ? 0 : n);                             // m (P-ACO): this step's ratios
+    uint32_t* stage_c = reinterpret_cast<uint32_t*>(stage_r + (a.T ? 0 : a.m));  // 2m: this step's pairs
+    uint32_t* vis = stage_c + (a.T ? 0 : 2 * a.m);                    // nw
     if (threadIdx.x == 0) { ring->produced = 0; ring->consumed = 0; ring->stop = 0; }
     if (warp == 0) {
         if (!a.T)
@@ -95,21 +107,20 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
         // the generator (rng.hpp:40-50), state carried across iterations in a.rng
         uint64_t s[4];
         for (int q = 0; q < 4; ++q) s[q] = a.rng[(size_t)ant * 4 + q];
-        uint32_t p = 0;
-        for (;;) {
-            if ((p & 31u) == 0) {
-                if (p - ring->consumed >= kIrRing - 32) {  // keep the consumption checkpoint alive
-                    __threadfence_block();
-                    ring->produced = p;
-                    while (p - ring->consumed >= kIrRing - 32 && !ring->stop) __nanosleep(200);
-                }
-                if (ring->stop) return;
-                unsigned long long* c = ring->ckpt[(p >> 5) % kIrCkpt];
-                c[0] = s[0]; c[1] = s[1]; c[2] = s[2]; c[3] = s[3];
+        // batches of 32 draws: the checkpoint, then 32 unrolled steps with no test in
+        // between, so consecutive steps' independent work (the output of one, the state
+        // update of the next) overlaps
+        for (uint32_t p = 0;; p += 32) {
+            if (p - ring->consumed >= kIrRing - 32) {  // keep the consumption checkpoint alive
+                while (p - ring->consumed >= kIrRing - 32 && !ring->stop) __nanosleep(100);
             }
-            ring->draw[p % kIrRing] = xoshiro_next(s);
-            ++p;
-            if ((p & 31u) == 0) { __threadfence_block(); ring->produced = p; }
+            if (ring->stop) return;
+            unsigned long long* c = ring->ckpt[(p >> 5) % kIrCkpt];
+            c[0] = s[0]; c[1] = s[1]; c[2] = s[2]; c[3] = s[3];
+            unsigned long long* d = ring->draw + (p % kIrRing);
+#pragma unroll
+            for (int q = 0; q < 32; ++q) d[q] = xoshiro_next(s);
+            st_release_cta(&ring->produced, p + 32);  // the 32 draws before the count
         }
     }
     // ---- warp 0: the construction ----
@@ -117,9 +128,8 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     __syncwarp();
     uint32_t cidx = 0;  // draws consumed so far (warp-uniform)
     auto wait_for = [&](uint32_t upto) {  // draws [0, upto) are in the ring
-        if (lane == 0) while (ring->produced < upto) {}
+        if (lane == 0) while (ld_acquire_cta(&ring->produced) < upto) {}
         __syncwarp();
-        __threadfence_block();
     };
     auto take = [&]() -> uint64_t {  // next draw, lane 0's view (other lanes follow the index)
         wait_for(cidx + 1);
@@ -199,60 +209,99 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
             }
             ++n_forced;
         } else {
-            // ColonyPheromone::begin_step (construction.hpp:121-132): the 2m contributions
-            // (ant q's prev then next of cur) in order, 32 per pass, one lane each. Lanes
-            // that hit the same city are grouped (match.any) and the group's lowest lane
-            // adds them in lane order, so every acc[c] receives its terms in ant order -
-            // the fp64 sum order of the reference.
+            // ColonyPheromone::begin_step (construction.hpp:121-132). The 2m contributions
+            // (ant q's prev then next of cur) are fetched at once into a shared staging list,
+            // then applied 32 per pass, one lane each: lanes that hit the same city are grouped
+            // (match.any) and the group's lowest lane adds them in lane order, so every acc[c]
+            // receives its terms in ant order - the fp64 sum order of the reference.
             if (!a.T) {
+#pragma unroll 4
+                for (uint32_t q = lane; q < a.m; q += 32) {
+                    const double r = a.ratio[q];
+                    uint2 pr = make_uint2(kNone, kNone);
+                    if (r != 0.0) pr = a.nbr[(size_t)q * n + cur];
+                    stage_c[2 * q] = pr.x;
+                    stage_c[2 * q + 1] = pr.y;
+                    stage_r[q] = r;
+                }
+                __syncwarp();
                 for (uint32_t e0 = 0; e0 < 2 * a.m; e0 += 32) {
-                    const uint32_t e = e0 + lane, q = e >> 1;
-                    const double r = e < 2 * a.m ? a.ratio[q] : 0.0;
-                    uint32_t c = kNone;
-                    if (r != 0.0) {
-                        const uint2 pr = a.nbr[(size_t)q * n + cur];
-                        c = (e & 1u) ? pr.y : pr.x;
-                    }
-                    ring->stage[lane] = r;
+                    const uint32_t e = e0 + lane;
+                    const uint32_t c = e < 2 * a.m ? stage_c[e] : kNone;
                     const unsigned grp = __match_any_sync(kFull, c);
-                    __syncwarp();
                     if (c != kNone && (int)lane == __ffs(grp) - 1) {
                         double v = acc[c];
-                        for (unsigned g = grp; g; g &= g - 1) v += ring->stage[__ffs(g) - 1];
+                        for (unsigned g = grp; g; g &= g - 1) v += stage_r[(e0 + __ffs(g) - 1) >> 1];
                         acc[c] = v;
                     }
                     __syncwarp();
                 }
+                // mult_[c] = Power(alpha)(tau0 + acc[c]) for the touched cities
+                // (construction.hpp:131), stored negated in place of acc[c]: a touched
+                // city's acc is > 0, so the sign tells converted entries apart (lanes that
+                // share a city write the same value)
+                for (uint32_t e = lane; e < 2 * a.m; e += 32) {
+                    const uint32_t c = stage_c[e];
+                    if (c != kNone) {
+                        const double v = acc[c];
+                        if (v > 0.0) acc[c] = -power(a.alpha, __dadd_rn(a.tau0, v));
+                    }
+                }
+                __syncwarp();
             }
             const double2 qc = a.xy[cur];
             const double* trow = a.T ? a.T + (size_t)cur * n : nullptr;
             double best = -1.0;
             uint32_t bj = kNone;
             uint32_t cnt_total = 0;
-            for (uint32_t w = 0; w < nw; ++w) {
-                const uint32_t free_bits = ~vis[w];
-                if (!free_bits) continue;
-                const uint32_t cnt = __popc(free_bits);
-                cnt_total += cnt;
-                wait_for(cidx + cnt);  // one draw per candidate, ascending city index
-                if ((free_bits >> lane) & 1u) {
-                    const uint32_t j = w * 32 + lane;
-                    const uint64_t raw = ring->draw[(cidx + __popc(free_bits & ((1u << lane) - 1u))) % kIrRing];
-                    const double u = (double)(raw >> 11) * 0x1.0p-53;
-                    int32_t d = euc2d(qc, a.xy[j]);
-                    if (d < 1) d = 1;
-                    double eta = power(a.beta, 1.0 / (double)d);
-                    if (a.eta_table) eta = (double)(float)eta;
-                    double ta;
-                    if (trow) ta = power(a.alpha, trow[j]);
-                    else {
-                        const double aj = acc[j];
-                        ta = aj == 0.0 ? tau0_alpha : power(a.alpha, __dadd_rn(a.tau0, aj));
-                    }
-                    const double score = __dmul_rn(__dmul_rn(ta, eta), u);
-                    if (score > best) { best = score; bj = j; }
+            // one draw per unvisited city in ascending index; four bitmap words per pass so
+            // that four rows of eta / tau loads are in flight per lane
+            constexpr uint32_t U = 4;
+            const unsigned lt = (1u << lane) - 1u;
+            for (uint32_t w0 = 0; w0 < nw; w0 += U) {
+                uint32_t fb[U], cntv[U], tot = 0;
+#pragma unroll
+                for (uint32_t u = 0; u < U; ++u) {
+                    fb[u] = w0 + u < nw ? ~vis[w0 + u] : 0u;
+                    cntv[u] = __popc(fb[u]);
+                    tot += cntv[u];
                 }
-                cidx += cnt;
+                if (tot == 0) continue;
+                double eta[U], ta[U];
+#pragma unroll
+                for (uint32_t u = 0; u < U; ++u) {
+                    eta[u] = 0.0; ta[u] = 0.0;
+                    if ((fb[u] >> lane) & 1u) {
+                        const uint32_t j = (w0 + u) * 32 + lane;
+                        if (a.eta_tab) {
+                            eta[u] = (double)a.eta_tab[(size_t)cur * n + j];
+                        } else {
+                            int32_t d = euc2d(qc, a.xy[j]);
+                            if (d < 1) d = 1;
+                            eta[u] = power(a.beta, 1.0 / (double)d);
+                            if (a.eta_table) eta[u] = (double)(float)eta[u];
+                        }
+                        if (trow) ta[u] = power(a.alpha, trow[j]);
+                        else {
+                            const double aj = acc[j];
+                            ta[u] = aj == 0.0 ? tau0_alpha : -aj;
+                        }
+                    }
+                }
+                wait_for(cidx + tot);
+                uint32_t off = cidx;
+#pragma unroll
+                for (uint32_t u = 0; u < U; ++u) {
+                    if ((fb[u] >> lane) & 1u) {
+                        const uint64_t raw = ring->draw[(off + __popc(fb[u] & lt)) % kIrRing];
+                        const double uu = (double)(raw >> 11) * 0x1.0p-53;
+                        const double score = __dmul_rn(__dmul_rn(ta[u], eta[u]), uu);
+                        if (score > best) { best = score; bj = (w0 + u) * 32 + lane; }
+                    }
+                    off += cntv[u];
+                }
+                cidx += tot;
+                cnt_total += tot;
                 if (lane == 0) ring->consumed = cidx;
             }
             // warp argmax, strict >, lowest city index on equal scores
@@ -265,12 +314,10 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
             next = bj;
             n_cmp += cnt_total;  // construction.hpp:275
             if (!a.T) {
-                // ColonyPheromone::end_step: reset the touched entries
-                for (uint32_t q = lane; q < a.m; q += 32) {
-                    if (a.ratio[q] == 0.0) continue;
-                    const uint2 pr = a.nbr[(size_t)q * n + cur];
-                    acc[pr.x] = 0.0;
-                    acc[pr.y] = 0.0;
+                // ColonyPheromone::end_step: reset the touched entries (from the staging list)
+                for (uint32_t e = lane; e < 2 * a.m; e += 32) {
+                    const uint32_t c = stage_c[e];
+                    if (c != kNone) acc[c] = 0.0;
                 }
                 __syncwarp();
             }
@@ -308,6 +355,17 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
         atomicAdd(&a.counters[8], n_cmp);
         if (do2) atomicAdd(&a.counters[9], 1ull);
     }
+}
+
+// Heuristic's table (construction.hpp:52-61): eta^beta of every pair as f32, the same
+// expression the construction would otherwise evaluate per candidate and step
+__global__ void k_eta_table(const double2* __restrict__ xy, uint32_t n, double beta, float* __restrict__ tab) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)n * n) return;
+    const uint32_t i = (uint32_t)(idx / n), j = (uint32_t)(idx % n);
+    int32_t d = euc2d(xy[i], xy[j]);
+    if (d < 1) d = 1;
+    tab[idx] = (float)power(beta, 1.0 / (double)d);
 }
 
 // ratios snapshot (Colony::snapshot_ratios, colony.hpp:159-167)

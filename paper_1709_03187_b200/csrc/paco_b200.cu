@@ -91,12 +91,13 @@ struct paco_handle {
     uint64_t* rng = nullptr;   // m*4 xoshiro256++ states
     double* ratio = nullptr;   // m
     double* Tfull = nullptr;   // classic: n*n
+    float* eta_tab = nullptr;  // n*n eta^beta f32 (n <= 5000)
 
     ~paco_handle() {
         if (dev >= 0) cudaSetDevice(dev);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
                         partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words,
-                        scratch_u32, scratch_u64, rng, ratio, Tfull};
+                        scratch_u32, scratch_u64, rng, ratio, Tfull, eta_tab};
         for (void* p : ptrs)
             if (p) cudaFree(p);
         for (auto e : evpool) cudaEventDestroy(e);
@@ -188,8 +189,8 @@ static paco_status build_grid(paco_handle* h) {
 }
 
 // reference rule: [draw ring] [acc n doubles (P-ACO)] [bitmap]
-static size_t ir_smem_bytes(uint32_t n, uint32_t nwords, int mode) {
-    return sizeof(IrRing) + (mode == PACO_MODE_CLASSIC ? 0 : (size_t)8 * n) + (size_t)nwords * 4;
+static size_t ir_smem_bytes(uint32_t n, uint32_t m, uint32_t nwords, int mode) {
+    return sizeof(IrRing) + (mode == PACO_MODE_CLASSIC ? 0 : (size_t)8 * n + (size_t)16 * m) + (size_t)nwords * 4;
 }
 
 // colony state shared by both selection rules
@@ -255,6 +256,11 @@ static paco_status setup_ir(paco_handle* h) {
     CU(cudaMemcpy(h->rng, st.data(), sizeof(uint64_t) * st.size(), cudaMemcpyHostToDevice));
     CU(dalloc(&h->ratio, m));
     CU(cudaMemset(h->ratio, 0, sizeof(double) * m));
+    if (n <= 5000) {  // the reference keeps eta^beta in an f32 table for these sizes
+        CU(dalloc(&h->eta_tab, (size_t)n * n));
+        k_eta_table<<<(unsigned)(((size_t)n * n + 255) / 256), 256, 0, h->st>>>(h->xy, n, h->cfg.beta, h->eta_tab);
+        CU(cudaGetLastError());
+    }
     if (h->mode == PACO_MODE_CLASSIC) {  // PheromoneMatrix(n, rho, tau_max), construction.hpp:165-175
         CU(dalloc(&h->Tfull, (size_t)n * n));
         std::vector<double> init((size_t)n * n, h->cfg.tau_max);
@@ -353,7 +359,7 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
     const uint32_t kk = std::min<uint32_t>(cfg->candidates, n - 1), kpp = (kk + 1) & ~1u;
     (void)kpp;
     const bool ir = cfg->rule == PACO_RULE_INDEPENDENT_ROULETTE;
-    const size_t smem_need = ir ? ir_smem_bytes(n, nwords, mode) : kFbList * 4 + (size_t)nwords * 4;
+    const size_t smem_need = ir ? ir_smem_bytes(n, cfg->ants, nwords, mode) : kFbList * 4 + (size_t)nwords * 4;
     if (!ir && n >= (1u << 21))  // the pick packs city ids into 21 bits (implied by the bitmap bound below)
         return fail(PACO_E_UNSUPPORTED, "visited bitmap exceeds shared memory (n too large)");
     if (smem_need > (size_t)prop.sharedMemPerBlockOptin)
@@ -448,8 +454,9 @@ static paco_status launch_construct_ir(paco_handle* h, bool seeding) {
     a.seeding = seeding ? 1 : 0;
     a.coin_always = 0;
     a.eta_table = h->n <= 5000 ? 1 : 0;  // Heuristic keeps an f32 table iff the instance has a matrix
+    a.eta_tab = h->eta_tab;
     a.two_opt_prob = h->cfg.two_opt_prob; a.two_opt_window = h->cfg.two_opt_window;
-    const size_t smem = ir_smem_bytes(h->n, h->nwords, h->mode);
+    const size_t smem = ir_smem_bytes(h->n, h->m, h->nwords, h->mode);
     if (smem > 48 * 1024)
         CU(cudaFuncSetAttribute(k_construct_ir, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_construct_ir<<<h->m, 64, smem, h->st>>>(a);
