@@ -242,6 +242,6 @@ def run(inst: Instance, cfg: RunConfig, mode: Mode = Mode.partial_aco) -> RunRep
 def run_timed_baseline(inst: Instance, cfg: RunConfig, budget_s: float) -> RunReport:
     """engine.hpp:339-344"""
     if budget_s <= 0.0:
-        raise ValueError("budget must be positive")
+        raise N.InvalidArgument(N.PACO_E_INVALID, "budget must be positive")
     from dataclasses import replace
     return run(inst, replace(cfg, time_budget_s=budget_s), Mode.paco_full)

@@ -89,6 +89,21 @@ def test_optima_and_grid442():
         load_optima("x -1\n")
 
 
+def test_reference_test_instance_generator():
+    """tests/refgen.py reproduces oracles.hpp:123-131 (std::mt19937_64 + uniform_real_distribution,
+    libstdc++): values printed by a g++ 13 build of the same calls."""
+    from refgen import MT19937_64, random_instance
+    g = MT19937_64()
+    for _ in range(9999):
+        g()
+    assert g() == 9981545732273789042  # [rand.predef]: 10000th output of the default-seeded engine
+    g3 = MT19937_64(3)
+    assert (g3(), g3()) == (10307413207671831467, 3611203882987592167)
+    inst = random_instance(MT19937_64(3), 3)
+    assert inst.xs.tolist() == [195.76375476116183, 346.36890921172545, 361.30268965844164]
+    assert inst.ys.tolist() == [558.76598962317905, 590.24127156131578, 559.79563654389858]
+
+
 def test_config_instances_shapes_and_determinism():
     for name, spec in CONFIGS.items():
         small = make_config_instance(name, n=2000)
