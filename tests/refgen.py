@@ -64,3 +64,27 @@ def random_instance(gen: MT19937_64, n: int, box: float = 1000.0, name: str = "r
         ys[i] = uniform_real(gen, 0.0, box)
         xs[i] = uniform_real(gen, 0.0, box)
     return Instance(name, xs, ys)
+
+
+def held_karp(inst: Instance) -> int:
+    """Exact optimum by the Held–Karp subset DP (the reference tests' oracle::held_karp), over
+    TSPLIB EUC_2D distances; masks are processed layer by layer with numpy."""
+    n = inst.n
+    d = np.array([[inst.dist(i, j) for j in range(n)] for i in range(n)], np.int64)
+    m = n - 1  # city 0 is the fixed start; bit k stands for city k + 1
+    full = 1 << m
+    inf = np.iinfo(np.int64).max // 4
+    dp = np.full((full, m), inf, np.int64)
+    for k in range(m):
+        dp[1 << k, k] = d[0, k + 1]
+    masks = np.arange(full)
+    pop = np.array([bin(x).count("1") for x in range(full)])
+    for size in range(1, m):
+        layer = masks[pop == size]
+        for j in range(m):
+            src = layer[(layer >> j) & 1 == 1]
+            for k in range(m):
+                tgt = src[(src >> k) & 1 == 0]
+                nxt = tgt | (1 << k)  # distinct for a fixed (j, k), so plain fancy indexing is safe
+                dp[nxt, k] = np.minimum(dp[nxt, k], dp[tgt, j] + d[j + 1, k + 1])
+    return int(min(dp[full - 1, j] + d[j + 1, 0] for j in range(m)))

@@ -144,3 +144,85 @@ def test_sweep_end_to_end(tmp_path):
     assert [r.mode for r in back] == ["paco", "partial", "partial"]
     assert (tmp_path / "smoke_runs.csv").read_text().count("\n") == 7
     assert "baseline (paco_full)" in log.getvalue()
+
+
+# ------------------------------------------------------------------ test_bench.cpp:217-346, case for case
+
+def write_instance(tmp_path, inst) -> str:
+    p = tmp_path / f"{inst.name}.tsp"
+    p.write_text(emit_tsplib(inst))
+    return str(p)
+
+
+@pytest.mark.gpu
+def test_run_experiment_sweeps_a_grid_and_writes_reports(tmp_path):
+    """test_bench.cpp:217-271, on the same 16-city instance (tests/refgen.py) with its Held–Karp optimum."""
+    from refgen import MT19937_64, held_karp, random_instance
+    inst = random_instance(MT19937_64(5), 16, 300.0, "mini")
+    path = write_instance(tmp_path, inst)
+    (tmp_path / "optima.txt").write_text(f"mini {held_karp(inst)}\n")
+    spec = X.ExperimentSpec(label="smoke", instance_paths=[path], optima_path=str(tmp_path / "optima.txt"), trials=2,
+                            max_mod_grid=[1.0, 0.5], partial_prob_grid=[1.0], out_dir=str(tmp_path / "out"))
+    spec.base.ants, spec.base.iterations, spec.base.workers, spec.base.seed = 4, 60, 1, 42
+    spec.base.convergence_interval_s = 0.001
+    res = X.run_experiment(spec, io.StringIO())
+    assert len(res.rows) == 3 and res.rows[0].mode == "paco"  # 1 baseline row + 2 grid rows
+    assert len(res.records) == 6
+    for row in res.rows:
+        assert not row.error and row.trials == 2 and not math.isnan(row.err_mean)
+        assert row.err_best <= row.err_mean <= row.err_worst and row.err_sd >= 0.0
+        assert row.err_best >= 0.0  # Held–Karp is exact
+    assert res.rows[1].speedup > 0.0
+    out = tmp_path / "out"
+    assert (out / "smoke_summary.csv").exists() and (out / "smoke_runs.csv").exists() and (out / "conv").is_dir()
+    back = X.read_summary_csv((out / "smoke_summary.csv").read_text())
+    assert len(back) == 3
+    for b, r in zip(back, res.rows):  # %.17g round trip is exact
+        assert b.err_mean == r.err_mean and b.time_mean_s == r.time_mean_s and b.speedup == r.speedup
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rule", ["roulette", "independent"])
+def test_sweeps_are_deterministic_for_a_fixed_master_seed(tmp_path, rule):
+    """test_bench.cpp:273-306"""
+    from refgen import MT19937_64, random_instance
+    path = write_instance(tmp_path, random_instance(MT19937_64(7), 18, 400.0, "det"))
+    spec = X.ExperimentSpec(label="det", instance_paths=[path], trials=3, include_baseline=False,
+                            max_mod_grid=[1.0, 0.3])
+    spec.base.ants, spec.base.iterations, spec.base.workers, spec.base.seed, spec.base.rule = 4, 80, 1, 7, rule
+    a = X.run_experiment(spec, io.StringIO())
+    b = X.run_experiment(spec, io.StringIO())
+    assert len(a.records) == len(b.records) == 6
+    for x, y in zip(a.records, b.records):
+        assert (x.best_length, x.comparisons, x.seed) == (y.best_length, y.comparisons, y.seed)
+    spec.base.seed = 8  # fresh seeds shift results
+    c = X.run_experiment(spec, io.StringIO())
+    assert any(x.comparisons != z.comparisons for x, z in zip(a.records, c.records))
+
+
+@pytest.mark.gpu
+def test_timed_baseline_pairing_produces_a_time_budget_row(tmp_path):
+    """test_bench.cpp:308-333"""
+    from refgen import MT19937_64, random_instance
+    path = write_instance(tmp_path, random_instance(MT19937_64(9), 20, 400.0, "timed"))
+    spec = X.ExperimentSpec(label="timed", instance_paths=[path], trials=1, include_baseline=False,
+                            timed_baseline=True)
+    spec.base.ants, spec.base.iterations, spec.base.workers, spec.base.seed = 2, 300, 1, 3
+    res = X.run_experiment(spec, io.StringIO())
+    assert len(res.rows) == 2
+    assert res.rows[0].pairing == X.EQUAL_ITERATIONS and res.rows[1].pairing == X.TIME_BUDGET
+    assert res.rows[1].mode == "paco_timed"
+    assert res.rows[1].iters_mean >= 1.0 and res.rows[1].speedup > 0.0
+
+
+def test_experiment_validation_catches_bad_specs():
+    """test_bench.cpp:335-346"""
+    spec = X.ExperimentSpec(instance_paths=["/definitely/not/here.tsp"])
+    with pytest.raises(ValueError):
+        spec.validate()
+    spec.instance_paths = []
+    with pytest.raises(ValueError):
+        spec.validate()
+    spec.trials = 0
+    with pytest.raises(ValueError):
+        spec.validate()
