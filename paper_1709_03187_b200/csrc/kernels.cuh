@@ -3,8 +3,12 @@
 #pragma once
 #include "device.cuh"
 
+#if defined(PACO_TIMING) || defined(PACO_SPECSTAT) || defined(PACO_PHASES)
+#define PACO_DEBUG_SYMS
+#endif
+
 namespace pacob200 {
-#ifdef PACO_TIMING
+#ifdef PACO_DEBUG_SYMS
 __device__ unsigned long long g_timing[16];
 __device__ unsigned long long g_prof[96];  // ant 0 profile by tour position (20 buckets)
 #endif
@@ -601,6 +605,9 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         const uint4 v = philox10(make_uint4(slot >> 2, ant, (uint32_t)iter, (uint32_t)(iter >> 32)), key);
         return pick_word(v, slot & 3);
     };
+#ifdef PACO_PHASES
+    const long long ph0 = clock64();
+#endif
     for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
     __syncwarp();
     if (lane == 0 && (n & 31)) vis[nw - 1] = 0xffffffffu << (n & 31);  // padding bits count as visited
@@ -628,12 +635,7 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
     } else {
         // construction.hpp:322-333: copy the cyclic preserved segment of l_best
         const uint32_t preserved = n - m_mod;
-        for (uint32_t t = lane; t < preserved; t += 32) {
-            uint32_t p = start_pos + t; if (p >= n) p -= n;
-            const uint32_t city = lb[p];
-            out[t] = city;
-            atomicOr(&vis[city >> 5], 1u << (city & 31));
-        }
+        warp_copy_segment(out, lb, n, start_pos, preserved, vis, lane);
         if (preserved == 0) {
             const uint32_t anchor = lb[start_pos];
             if (lane == 0) { out[0] = anchor; vis[anchor >> 5] |= 1u << (anchor & 31); }
@@ -646,6 +648,9 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
     }
     __syncwarp();
 
+#ifdef PACO_PHASES
+    const long long ph1 = clock64();
+#endif
     uint32_t n_fb = 0, n_tie = 0;
     const uint32_t n_dec = n - pos;       // decisions of this construction (the last one forced)
     // shared-window addresses pinned in registers (an opaque move keeps the compiler from
@@ -751,6 +756,29 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
                 // decision's probe does not depend on it.
                 sts_u32_if(vw_addr, vw | bit, lane == r);
                 n_tie += tie ? 1u : 0u;
+#ifdef PACO_SPECSTAT
+                {
+                    const uint32_t mx = __reduce_max_sync(kFull, lane_in ? e.y : 0u);
+                    const int tl = __ffs(__ballot_sync(kFull, lane_in && e.y == mx)) - 1;
+                    const uint32_t top = __shfl_sync(kFull, e.x, tl);
+                    const uint32_t mx2 = __reduce_max_sync(kFull, (lane_in && lane != (uint32_t)tl) ? e.y : 0u);
+                    const int tl2 = __ffs(__ballot_sync(kFull, lane_in && lane != (uint32_t)tl && e.y == mx2)) - 1;
+                    const uint32_t top2 = __shfl_sync(kFull, e.x, tl2);
+                    const uint32_t mf = __reduce_max_sync(kFull, __float_as_uint(w));
+                    const int fl = __ffs(__ballot_sync(kFull, w > 0.0f && __float_as_uint(w) == mf)) - 1;
+                    const uint32_t topf = __shfl_sync(kFull, e.x, fl);
+                    if (lane == 0) {
+                        atomicAdd(&g_timing[4], 1ull);
+                        if (next == top) atomicAdd(&g_timing[5], 1ull);
+                        if (next == top || next == top2) atomicAdd(&g_timing[6], 1ull);
+                        if (next == topf) atomicAdd(&g_timing[7], 1ull);
+                        if (!partial) {
+                            atomicAdd(&g_timing[8], 1ull);
+                            if (next == top) atomicAdd(&g_timing[9], 1ull);
+                        }
+                    }
+                }
+#endif
 #ifdef PACO_SEG
                 const long long sg3 = seg_clk(next);
                 sq_tail += sg0 - sq_prev; sq_probe += sg1 - sg0; sq_scan += sg2 - sg1; sq_pick += sg3 - sg2; ++sq_n;
@@ -821,6 +849,9 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         }
     }
 #endif
+#ifdef PACO_PHASES
+    const long long ph2 = clock64();
+#endif
     // maybe_two_opt (two_opt.hpp:71-76): draw slot 3
     uint32_t n_2opt = 0;
     if (!a.force && a.two_opt_prob > 0.0 && u01_f64(word(3)) < a.two_opt_prob) {
@@ -828,13 +859,7 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         n_2opt = 1;
     }
     // tour length (instance.hpp:120-127), int64, warp-parallel over positions
-    long long len = 0;
-    for (uint32_t p = lane; p < n; p += 32) {
-        const uint32_t c0 = out[p], c1 = out[p + 1 < n ? p + 1 : 0];
-        len += euc2d(a.xy[c0], a.xy[c1]);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) len += __shfl_xor_sync(kFull, len, off);
+    const long long len = warp_tour_length(out, n, a.xy, lane);
     if (a.validate) {
         // permutation check (instance.hpp:109-117) reusing the bitmap
         for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
@@ -848,6 +873,17 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         }
         if (__any_sync(kFull, bad) && lane == 0) atomicExch(a.err, 1);
     }
+#ifdef PACO_PHASES
+    if (lane == 0) {
+        const long long ph3 = clock64();
+        const int o = partial ? 5 : 0;
+        atomicAdd(&g_timing[o + 0], (unsigned long long)(ph1 - ph0));
+        atomicAdd(&g_timing[o + 1], (unsigned long long)(ph2 - ph1));
+        atomicAdd(&g_timing[o + 2], (unsigned long long)(ph3 - ph2));
+        atomicAdd(&g_timing[o + 3], (unsigned long long)n_dec);
+        atomicAdd(&g_timing[o + 4], 1ull);
+    }
+#endif
     partial_out = partial;
     cnt[0] = n_dec; cnt[1] = n_fb; cnt[2] = n_tie; cnt[3] = n_forced; cnt[4] = n_2opt;
     return len;

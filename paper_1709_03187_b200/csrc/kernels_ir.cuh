@@ -166,12 +166,7 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
         pos = 1; cur = start; remaining = n - 1;
     } else {
         const uint32_t preserved = n - m_mod;
-        for (uint32_t t = lane; t < preserved; t += 32) {
-            uint32_t p = start_pos + t; if (p >= n) p -= n;
-            const uint32_t city = lb[p];
-            out[t] = city;
-            atomicOr(&vis[city >> 5], 1u << (city & 31));
-        }
+        warp_copy_segment(out, lb, n, start_pos, preserved, vis, lane);
         if (preserved == 0) {
             const uint32_t anchor = lb[start_pos];
             if (lane == 0) { out[0] = anchor; vis[anchor >> 5] |= 1u << (anchor & 31); }
@@ -342,10 +337,7 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     }
     __syncwarp();
     if (do2) two_opt_warp(out, n, a.two_opt_window, a.xy, lane);
-    long long len = 0;
-    for (uint32_t p = lane; p < n; p += 32) len += euc2d(a.xy[out[p]], a.xy[out[p + 1 < n ? p + 1 : 0]]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) len += __shfl_xor_sync(kFull, len, off);
+    const long long len = warp_tour_length(out, n, a.xy, lane);
     if (lane == 0) {
         a.new_len[ant] = len;
         a.partial_flag[ant] = (uint8_t)partial;

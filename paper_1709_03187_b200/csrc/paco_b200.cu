@@ -754,7 +754,7 @@ paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, u
     return PACO_OK;
 }
 
-#ifdef PACO_TIMING
+#ifdef PACO_DEBUG_SYMS
 extern "C" void paco_debug_prof(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 96); }
 extern "C" void paco_debug_timing(unsigned long long* out, int reset) {
     cudaMemcpyFromSymbol(out, g_timing, sizeof(unsigned long long) * 16);
