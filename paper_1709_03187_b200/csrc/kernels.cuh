@@ -3,7 +3,7 @@
 #pragma once
 #include "device.cuh"
 
-#if defined(PACO_TIMING) || defined(PACO_SPECSTAT) || defined(PACO_PHASES)
+#if defined(PACO_TIMING) || defined(PACO_SPECSTAT) || defined(PACO_PHASES) || defined(PACO_IRSEG)
 #define PACO_DEBUG_SYMS
 #endif
 

@@ -97,8 +97,10 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     uint32_t* vis = stage_c + (a.T ? 0 : 2 * a.m);                    // nw
     if (threadIdx.x == 0) { ring->produced = 0; ring->consumed = 0; ring->stop = 0; }
     if (warp == 0) {
-        if (!a.T)
+        if (!a.T) {
             for (uint32_t j = lane; j < n; j += 32) acc[j] = 0.0;
+            for (uint32_t q = lane; q < a.m; q += 32) stage_r[q] = a.ratio[q];  // fixed for the iteration
+        }
         for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
     }
     __syncthreads();
@@ -127,9 +129,18 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     if (lane == 0 && (n & 31)) vis[nw - 1] = 0xffffffffu << (n & 31);
     __syncwarp();
     uint32_t cidx = 0;  // draws consumed so far (warp-uniform)
+#ifdef PACO_IRSEG
+    long long sg_wait = 0, sg_begin = 0, sg_scan = 0, sg_end = 0, sg_stage = 0, sg_group = 0;
+#endif
     auto wait_for = [&](uint32_t upto) {  // draws [0, upto) are in the ring
+#ifdef PACO_IRSEG
+        const long long w0c = clock64();
+#endif
         if (lane == 0) while (ld_acquire_cta(&ring->produced) < upto) {}
         __syncwarp();
+#ifdef PACO_IRSEG
+        sg_wait += clock64() - w0c;
+#endif
     };
     auto take = [&]() -> uint64_t {  // next draw, lane 0's view (other lanes follow the index)
         wait_for(cidx + 1);
@@ -204,6 +215,9 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
             }
             ++n_forced;
         } else {
+#ifdef PACO_IRSEG
+            const long long b0c = clock64();
+#endif
             // ColonyPheromone::begin_step (construction.hpp:121-132). The 2m contributions
             // (ant q's prev then next of cur) are fetched at once into a shared staging list,
             // then applied 32 per pass, one lane each: lanes that hit the same city are grouped
@@ -212,25 +226,40 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
             if (!a.T) {
 #pragma unroll 4
                 for (uint32_t q = lane; q < a.m; q += 32) {
-                    const double r = a.ratio[q];
                     uint2 pr = make_uint2(kNone, kNone);
-                    if (r != 0.0) pr = a.nbr[(size_t)q * n + cur];
+                    if (stage_r[q] != 0.0) pr = a.nbr[(size_t)q * n + cur];
                     stage_c[2 * q] = pr.x;
                     stage_c[2 * q + 1] = pr.y;
-                    stage_r[q] = r;
                 }
                 __syncwarp();
+#ifdef PACO_IRSEG
+                const long long bAc = clock64();
+                sg_stage += bAc - b0c;
+#endif
                 for (uint32_t e0 = 0; e0 < 2 * a.m; e0 += 32) {
                     const uint32_t e = e0 + lane;
                     const uint32_t c = e < 2 * a.m ? stage_c[e] : kNone;
+                    const unsigned live = __ballot_sync(kFull, c != kNone);
+                    if (!live) continue;  // no l_best tour yet (seeding) or no ratio
                     const unsigned grp = __match_any_sync(kFull, c);
-                    if (c != kNone && (int)lane == __ffs(grp) - 1) {
-                        double v = acc[c];
-                        for (unsigned g = grp; g; g &= g - 1) v += stage_r[(e0 + __ffs(g) - 1) >> 1];
-                        acc[c] = v;
+                    const bool leader = c != kNone && (int)lane == __ffs(grp) - 1;
+                    // each group's leader adds its members' terms in lane order: a serial
+                    // fp64 chain of predicated adds over broadcast loads that do not depend on
+                    // the sum, so the loads are in flight ahead of the chain
+                    double v = leader ? acc[c] : 0.0;
+                    const double* sr = stage_r + (e0 >> 1);
+                    const uint32_t nt = 2 * a.m - e0;  // terms in this pass (may exceed 32)
+#pragma unroll
+                    for (uint32_t src = 0; src < 32; ++src) {
+                        const double x = src < nt ? sr[src >> 1] : 0.0;
+                        if ((grp >> src) & 1u) v = __dadd_rn(v, x);
                     }
+                    if (leader) acc[c] = v;
                     __syncwarp();
                 }
+#ifdef PACO_IRSEG
+                sg_group += clock64() - bAc;
+#endif
                 // mult_[c] = Power(alpha)(tau0 + acc[c]) for the touched cities
                 // (construction.hpp:131), stored negated in place of acc[c]: a touched
                 // city's acc is > 0, so the sign tells converted entries apart (lanes that
@@ -244,6 +273,10 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
                 }
                 __syncwarp();
             }
+#ifdef PACO_IRSEG
+            const long long b1c = clock64();
+            sg_begin += b1c - b0c;
+#endif
             const double2 qc = a.xy[cur];
             const double* trow = a.T ? a.T + (size_t)cur * n : nullptr;
             double best = -1.0;
@@ -263,14 +296,32 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
                 }
                 if (tot == 0) continue;
                 double eta[U], ta[U];
+                if (a.eta_tab) {
+                    // every global load of the pass is issued before the first use (predicated
+                    // PTX loads; left to the compiler, each conversion sat right behind its load
+                    // and a pass made U serial L2 round trips)
+                    const size_t j0 = (size_t)w0 * 32 + lane;
+                    const float* erow = a.eta_tab + (size_t)cur * n + j0;
+                    float ef[U];
+                    double tv[U];
+#pragma unroll
+                    for (uint32_t u = 0; u < U; ++u) {
+                        const bool f = (fb[u] >> lane) & 1u;
+                        ef[u] = ldg_f32_if(erow + u * 32, f);
+                        tv[u] = trow ? ldg_f64_if(trow + j0 + u * 32, f) : (f ? acc[j0 + u * 32] : 0.0);
+                    }
+#pragma unroll
+                    for (uint32_t u = 0; u < U; ++u) {
+                        eta[u] = (double)ef[u];
+                        ta[u] = trow ? power(a.alpha, tv[u]) : (tv[u] == 0.0 ? tau0_alpha : -tv[u]);
+                    }
+                } else
 #pragma unroll
                 for (uint32_t u = 0; u < U; ++u) {
                     eta[u] = 0.0; ta[u] = 0.0;
                     if ((fb[u] >> lane) & 1u) {
                         const uint32_t j = (w0 + u) * 32 + lane;
-                        if (a.eta_tab) {
-                            eta[u] = (double)a.eta_tab[(size_t)cur * n + j];
-                        } else {
+                        {
                             int32_t d = euc2d(qc, a.xy[j]);
                             if (d < 1) d = 1;
                             eta[u] = power(a.beta, 1.0 / (double)d);
@@ -307,6 +358,10 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
                 if (b2 > best || (b2 == best && j2 < bj)) { best = b2; bj = j2; }
             }
             next = bj;
+#ifdef PACO_IRSEG
+            const long long b2c = clock64();
+            sg_scan += b2c - b1c;
+#endif
             n_cmp += cnt_total;  // construction.hpp:275
             if (!a.T) {
                 // ColonyPheromone::end_step: reset the touched entries (from the staging list)
@@ -316,6 +371,9 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
                 }
                 __syncwarp();
             }
+#ifdef PACO_IRSEG
+            sg_end += clock64() - b2c;
+#endif
         }
         ++n_dec;
         if (lane == 0) { out[pos] = next; vis[next >> 5] |= 1u << (next & 31); }
@@ -323,6 +381,14 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
         ++pos;
         cur = next;
     }
+#ifdef PACO_IRSEG
+    if (lane == 0) {
+        atomicAdd(&g_timing[0], (unsigned long long)sg_begin); atomicAdd(&g_timing[1], (unsigned long long)sg_scan);
+        atomicAdd(&g_timing[2], (unsigned long long)sg_wait); atomicAdd(&g_timing[3], (unsigned long long)sg_end);
+        atomicAdd(&g_timing[4], n_dec); atomicAdd(&g_timing[5], n_cmp);
+        atomicAdd(&g_timing[6], (unsigned long long)sg_stage); atomicAdd(&g_timing[7], (unsigned long long)sg_group);
+    }
+#endif
     // maybe_two_opt consumes exactly one draw (two_opt.hpp:71-76)
     const uint32_t do2 = uniform() < a.two_opt_prob ? 1u : 0u;
     // stop the generator; the stream state after exactly cidx draws: the checkpoint at
