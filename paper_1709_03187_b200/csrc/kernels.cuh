@@ -964,8 +964,23 @@ __global__ void __launch_bounds__(32, 1) k_construct_async(ConstructArgs a, uint
             const uint8_t ns = (uint8_t)(1 - st.lb_sel[ant]);
             const uint32_t* t = a.tours + ((size_t)ant * 2 + ns) * n;
             uint2* nb = st.nbr + (size_t)ant * n;
-            for (uint32_t p = lane; p < n; p += 32)
-                nb[t[p]] = make_uint2(t[p == 0 ? n - 1 : p - 1], t[p + 1 == n ? 0 : p + 1]);
+            // Ant::publish (colony.hpp:39-52): eight positions per lane per pass, all loads
+            // issued before the scattered stores
+            constexpr int U = 8;
+            for (uint32_t b = 0; b < n; b += 32 * U) {
+                uint32_t c[U], pv[U], nx[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const uint32_t p = b + 32 * j + lane;
+                    const bool in = p < n;
+                    c[j] = in ? t[p] : 0u;
+                    pv[j] = in ? t[p == 0 ? n - 1 : p - 1] : 0u;
+                    nx[j] = in ? t[p + 1 == n ? 0 : p + 1] : 0u;
+                }
+#pragma unroll
+                for (int j = 0; j < U; ++j)
+                    if (b + 32 * j + lane < n) nb[c[j]] = make_uint2(pv[j], nx[j]);
+            }
             __syncwarp();
             if (lane == 0) {
                 __threadfence();  // the slice before the length that makes it count
