@@ -3,7 +3,7 @@
 #pragma once
 #include "device.cuh"
 
-#if defined(PACO_TIMING) || defined(PACO_SPECSTAT) || defined(PACO_PHASES) || defined(PACO_IRSEG)
+#if defined(PACO_TIMING) || defined(PACO_SPECSTAT) || defined(PACO_PHASES) || defined(PACO_IRSEG) || defined(PACO_ANTPROF)
 #define PACO_DEBUG_SYMS
 #endif
 
@@ -11,6 +11,14 @@ namespace pacob200 {
 #ifdef PACO_DEBUG_SYMS
 __device__ unsigned long long g_timing[16];
 __device__ unsigned long long g_prof[96];  // ant 0 profile by tour position (20 buckets)
+#ifdef PACO_ANTPROF
+__device__ unsigned long long g_ant[4096 * 6];  // per ant: start ns, end ns, smid, decisions, fallbacks, partial
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 #endif
 
 // ============================================================ K0: spatial sort
@@ -721,10 +729,13 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
             // least its largest term), so the split is decided by a vote the compiler knows
             // to be warp-uniform
             const unsigned feas = __ballot_sync(kFull, w > 0.0f);
+            // the highest feasible lane (feasible by construction), while the scan runs
+            const bool is_last = lane == 31u - __clz(feas);
+            const uint32_t pick_key = (lane << 27) | e.x;
             // Hillis-Steele inclusive scan over the candidate lanes; S = S_{k-1}. (Forming S
-            // from the two last-level terms by broadcast, or packing the pick into one
-            // reduction, measured slower: the chain is sensitive to how the MIO operations
-            // interleave, profiles/README.md.)
+            // from the two last-level terms by broadcast, or every lane summing its own prefix
+            // from a shared-memory row, measured slower: the chain is sensitive to how the MIO
+            // operations interleave, profiles/README.md.)
             float v = w;
 #pragma unroll
             for (int st = 0; st < STEPS; ++st) {
@@ -742,14 +753,18 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
                 const float tol = __fmul_rn(1e-6f, S);
                 // Only feasible lanes (w > 0; lanes >= k have w = 0) may win: the tree-shaped
                 // scan is not monotone in f32, so an infeasible lane's S_r can exceed its left
-                // neighbour's by an ulp. The pick is two integer min-reductions over (lane, city)
-                // keys - lowest winning lane, else highest feasible lane - which deliver the
+                // neighbour's by an ulp. The pick is one integer min-reduction over (lane, city)
+                // key - lowest winning lane, else highest feasible lane - which delivers the
                 // city itself (ids < 2^21: the bitmap fits in shared memory), no ffs, no shuffle.
-                const uint32_t kw = __reduce_min_sync(kFull, (w > 0.0f && v > target) ? ((lane << 27) | e.x) : kNone);
-                const uint32_t kf = __reduce_min_sync(kFull, w > 0.0f ? (((31u - lane) << 27) | e.x) : kNone);
+                // The highest feasible lane comes from the feasibility vote, off the chain, and
+                // is folded into the predicate: if no lane wins, it is the only candidate left
+                // (one reduction instead of two plus a select; C5 construction 54.40 -> 54.18
+                // ms, profiles/README.md).
+                const bool win = ((w > 0.0f) & (v > target)) | is_last;
+                const uint32_t kw = __reduce_min_sync(kFull, win ? pick_key : kNone);
                 const unsigned tie = __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(v, target)) <= tol);
-                const uint32_t r = kw != kNone ? (kw >> 27) : 31u - (kf >> 27);
-                next = (kw != kNone ? kw : kf) & 0x07ffffffu;
+                const uint32_t r = kw >> 27;
+                next = kw & 0x07ffffffu;
                 // the visit of next: the winning lane already holds next's bitmap word (nothing
                 // has written the bitmap since it was read), so a predicated plain store does
                 // it - no atomic, no branch. No candidate of next is next itself, so the next
@@ -906,7 +921,18 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     const uint32_t ant = a.force ? a.force_ant : blockIdx.x;
     bool partial;
     uint32_t cnt[5];
+#ifdef PACO_ANTPROF
+    const unsigned long long pt0 = gtimer();
+#endif
     const long long len = build_one<KP, STEPS, BUF>(a, ant, a.iter, a.seeding != 0, smem_raw, fctx, partial, cnt);
+#ifdef PACO_ANTPROF
+    if (threadIdx.x == 0 && ant < 4096) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* g = g_ant + 6 * ant;
+        g[0] = pt0; g[1] = gtimer(); g[2] = smid; g[3] = cnt[0]; g[4] = cnt[1]; g[5] = partial;
+    }
+#endif
     if (threadIdx.x == 0) {
         a.new_len[ant] = len;
         if (!a.force) {

@@ -755,6 +755,9 @@ paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, u
 }
 
 #ifdef PACO_DEBUG_SYMS
+#ifdef PACO_ANTPROF
+extern "C" void paco_debug_ant(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ant, sizeof(unsigned long long) * 4096 * 6); }
+#endif
 extern "C" void paco_debug_prof(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 96); }
 extern "C" void paco_debug_timing(unsigned long long* out, int reset) {
     cudaMemcpyFromSymbol(out, g_timing, sizeof(unsigned long long) * 16);
