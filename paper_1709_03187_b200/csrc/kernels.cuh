@@ -180,20 +180,57 @@ __global__ void __launch_bounds__(T) k_knn_cells(const double2* __restrict__ xy,
 }
 
 // ============================================================ K5: weight table
+// Per-city perfect hash of the candidate list (setup, once per instance): the multiplier
+// M_i maps the k <= 16 candidates of city i to distinct slots (c * M_i) >> 27 of 32, so
+// k_weights finds the candidate index of a neighbour with one shared-memory lookup
+// instead of k comparisons. Trial multipliers are odd SplitMix values of (i, trial);
+// success probability per trial is 1.04% at k = 16 (about 96 trials), 2^14 trials are
+// allowed; a city without one sets *fail and k_weights keeps the comparison loop.
+constexpr int kHashSlotBits = 5;
+__device__ __forceinline__ uint32_t cand_slot(uint32_t c, uint32_t M) { return (c * M) >> (32 - kHashSlotBits); }
+__global__ void k_cand_hash(const uint32_t* __restrict__ knn32, uint32_t n, int k, uint32_t* __restrict__ mult,
+                            int* __restrict__ fail) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t c[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) c[r] = r < k ? knn32[(size_t)i * kNearRow + r] : 0u;
+    for (uint32_t t = 0; t < (1u << 14); ++t) {
+        unsigned long long z = ((unsigned long long)i << 20 | t) + 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        const uint32_t M = (uint32_t)(z ^ (z >> 31)) | 1u;
+        uint32_t used = 0;
+        bool ok = true;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            if (r < k) {
+                const uint32_t bit = 1u << cand_slot(c[r], M);
+                ok &= (used & bit) == 0;
+                used |= bit;
+            }
+        }
+        if (ok) { mult[i] = M; return; }
+    }
+    mult[i] = 0;
+    atomicExch(fail, 1);
+}
+
 // Per iteration, for every candidate edge (i, c_r): tau = tau0 + sum over ants a in
 // ant order of ratio_a * [c_r in {prev_a(i), next_a(i)}]  (fp64, bit-identical to
 // ColonyPheromone::begin_step, construction.hpp:121-132, restricted to candidate
 // edges; ratios per colony.hpp:159-177), w = f32(Power(alpha)(tau)) * eta^beta (f32).
 // Classic mode reads tau from the candidate-edge pheromone table T instead.
 // Output: packed {c_r, w} rows, the only table the construction kernel reads.
-template <int KMAX, bool LIVE>
+template <int KMAX, bool LIVE, bool HASH>
 __global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__ knn32, const float* __restrict__ eta,
                                                  const uint2* __restrict__ nbr, const int64_t* __restrict__ lb_len,
                                                  const uint8_t* __restrict__ has_lb, const int64_t* __restrict__ g_len,
                                                  const unsigned long long* __restrict__ gkey,
-                                                 const double* __restrict__ T, uint32_t n, uint32_t m, int k,
+                                                 const double* __restrict__ T, const uint32_t* __restrict__ mult,
+                                                 uint32_t n, uint32_t m, int k,
                                                  int kp, double alpha, double tau0, uint2* __restrict__ cand) {
-    extern __shared__ double ratio[];
+    extern __shared__ double ratio[];  // m ratios | HASH: slot table [32][blockDim] u32, acc [KMAX][blockDim] f64
     if (!T) {
         // colony.hpp:159-177 ratios. In async mode (gkey != nullptr) the colony changes under
         // this pass: lengths and g_best are read past L1 (ld.cv), a snapshot at pass start.
@@ -214,14 +251,26 @@ __global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__
     double acc[KMAX];
 #pragma unroll
     for (int r = 0; r < KMAX; ++r) { c[r] = r < k ? knn32[(size_t)i * kNearRow + r] : kNone; acc[r] = 0.0; }
-    if (!T) {
-        // eight ants' pairs in flight per thread, then accumulated in ant order (the fp64 sum
-        // order of ColonyPheromone::begin_step). The slices are streamed once: evict-first in
-        // sync mode, read past L1 in async mode (LIVE), where ants rewrite them meanwhile.
+    if (HASH && !T) {
+        // The candidate index of a neighbour is one lookup in the city's perfect-hash table
+        // (k_cand_hash): slot entries hold (r << 27 | c_r), empty slots kNone, and the
+        // per-candidate sums live in shared memory (column t of [KMAX][blockDim]) so the
+        // add can address acc[r] with the r found. Every sum still takes its terms in ant
+        // order. The comparison loop below was ALU-bound (91% of the ALU pipe, 32 compares
+        // per ant and city; profiles/README.md).
+        const uint32_t t = threadIdx.x, bd = blockDim.x;
+        uint32_t* tab = reinterpret_cast<uint32_t*>(ratio + m);
+        double* accs = reinterpret_cast<double*>(tab + 32 * bd);
+        const uint32_t M = mult[i];
+#pragma unroll
+        for (int s = 0; s < 32; ++s) tab[s * bd + t] = kNone;
+#pragma unroll
+        for (int r = 0; r < KMAX; ++r) {
+            if (r < k) tab[cand_slot(c[r], M) * bd + t] = ((uint32_t)r << 27) | c[r];
+            accs[r * bd + t] = 0.0;
+        }
         constexpr uint32_t U = 8;
-        for (uint32_t a0 = 0; a0 < m; a0 += U) {
-            uint2 p[U];
-            double rr[U];
+        auto fetch = [&](uint32_t a0, uint2 (&p)[U], double (&rr)[U]) {
 #pragma unroll
             for (uint32_t u = 0; u < U; ++u) {
                 const uint32_t a = a0 + u;
@@ -229,15 +278,61 @@ __global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__
                 const uint2* src = &nbr[(size_t)a * n + i];
                 p[u] = rr[u] != 0.0 ? (LIVE ? __ldcv(src) : __ldcs(src)) : make_uint2(kNone, kNone);
             }
+        };
+        uint2 p[U], pn[U];
+        double rr[U], rrn[U];
+        fetch(0, p, rr);
+        for (uint32_t a0 = 0; a0 < m; a0 += U) {
+            if (a0 + U < m) fetch(a0 + U, pn, rrn);
 #pragma unroll
             for (uint32_t u = 0; u < U; ++u) {
-                if (rr[u] == 0.0) continue;
-#pragma unroll
-                for (int r = 0; r < KMAX; ++r) {
-                    if (c[r] == p[u].x) acc[r] = __dadd_rn(acc[r], rr[u]);
-                    if (c[r] == p[u].y) acc[r] = __dadd_rn(acc[r], rr[u]);
+                const uint32_t ex = tab[cand_slot(p[u].x, M) * bd + t], ey = tab[cand_slot(p[u].y, M) * bd + t];
+                if ((ex & 0x07ffffffu) == p[u].x) {
+                    double* q = accs + (ex >> 27) * bd + t;
+                    *q = __dadd_rn(*q, rr[u]);
+                }
+                if ((ey & 0x07ffffffu) == p[u].y) {
+                    double* q = accs + (ey >> 27) * bd + t;
+                    *q = __dadd_rn(*q, rr[u]);
                 }
             }
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) { p[u] = pn[u]; rr[u] = rrn[u]; }
+        }
+#pragma unroll
+        for (int r = 0; r < KMAX; ++r) acc[r] = accs[r * bd + t];
+    } else if (!T) {
+        // Pairs of eight ants per batch, accumulated in ant order (the fp64 sum order of
+        // ColonyPheromone::begin_step); the next batch's loads are issued before the current
+        // batch is accumulated, so eight pairs are always in flight (issuing and then
+        // accumulating left the loads idle during the 512 compare/add instructions of a
+        // batch: 1.49 -> see profiles/README.md). The slices are streamed once: evict-first
+        // in sync mode, read past L1 in async mode (LIVE), where ants rewrite them meanwhile.
+        // prev != next for n >= 3 (a tour of distinct cities), so a candidate matches at
+        // most one of them and one predicated add per candidate does both tests.
+        constexpr uint32_t U = 8;
+        auto fetch = [&](uint32_t a0, uint2 (&p)[U], double (&rr)[U]) {
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+                const uint32_t a = a0 + u;
+                rr[u] = a < m ? ratio[a] : 0.0;
+                const uint2* src = &nbr[(size_t)a * n + i];
+                p[u] = rr[u] != 0.0 ? (LIVE ? __ldcv(src) : __ldcs(src)) : make_uint2(kNone, kNone);
+            }
+        };
+        uint2 p[U], pn[U];
+        double rr[U], rrn[U];
+        fetch(0, p, rr);
+        for (uint32_t a0 = 0; a0 < m; a0 += U) {
+            if (a0 + U < m) fetch(a0 + U, pn, rrn);
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+#pragma unroll
+                for (int r = 0; r < KMAX; ++r)
+                    if ((c[r] == p[u].x) | (c[r] == p[u].y)) acc[r] = __dadd_rn(acc[r], rr[u]);
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) { p[u] = pn[u]; rr[u] = rrn[u]; }
         }
     }
 #pragma unroll

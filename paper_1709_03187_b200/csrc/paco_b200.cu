@@ -70,6 +70,7 @@ struct paco_handle {
     uint8_t *lb_sel = nullptr, *has_lb = nullptr, *improved = nullptr, *partial = nullptr;
     int64_t *new_len = nullptr, *lb_len = nullptr, *g_len = nullptr;
     uint2* nbr = nullptr;
+    uint32_t* cand_mult = nullptr;       // per-city candidate perfect-hash multipliers (k <= 16)
     uint2* cur_nbr = nullptr;
     double* T = nullptr;
     GBest* gb = nullptr;
@@ -97,7 +98,7 @@ struct paco_handle {
         if (dev >= 0) cudaSetDevice(dev);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
                         partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words,
-                        scratch_u32, scratch_u64, rng, ratio, Tfull, eta_tab};
+                        scratch_u32, scratch_u64, rng, ratio, Tfull, eta_tab, cand_mult};
         for (void* p : ptrs)
             if (p) cudaFree(p);
         for (auto e : evpool) cudaEventDestroy(e);
@@ -324,6 +325,18 @@ static paco_status setup(paco_handle* h) {
                                                                  (int)k, h->cfg.beta, h->knn, h->eta);
     }
     CU(cudaGetLastError());
+    if (h->mode != PACO_MODE_CLASSIC && k <= 16) {  // candidate perfect hashes for k_weights
+        int* dfail = nullptr;
+        CU(dalloc(&h->cand_mult, n)); CU(dalloc(&dfail, 1));
+        CU(cudaMemsetAsync(dfail, 0, sizeof(int), st));
+        k_cand_hash<<<nb, tb, 0, st>>>(h->knn, n, (int)k, h->cand_mult, dfail);
+        CU(cudaGetLastError());
+        int hf = 0;
+        CU(cudaMemcpyAsync(&hf, dfail, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        cudaFree(dfail);
+        if (hf) { cudaFree(h->cand_mult); h->cand_mult = nullptr; }  // keep the comparison loop
+    }
     CU(cudaEventRecord(e1, st));
     CU(cudaStreamSynchronize(st));
     float ms = 0;
@@ -415,21 +428,26 @@ static cudaEvent_t ev(paco_handle* h, size_t i) {
 static paco_status launch_weights(paco_handle* h, cudaStream_t stream = nullptr, const unsigned long long* gkey = nullptr) {
     const uint32_t n = h->n, tb = 256;
     if (!stream) stream = h->st;
-    const size_t smem = h->T ? 0 : sizeof(double) * h->m;
-    const int km = kmax_for(h->k);
     const double* T = h->mode == PACO_MODE_CLASSIC ? h->T : nullptr;
-#define LAUNCH_W2(KM, LIVE)                                                                                \
+    const int km = kmax_for(h->k);
+    const bool hash = !T && h->cand_mult != nullptr && km <= 16;  // perfect-hash lookup (k_cand_hash)
+    const size_t smem = T ? 0 : sizeof(double) * h->m + (hash ? (sizeof(uint32_t) * 32 + sizeof(double) * km) * tb : 0);
+#define LAUNCH_W3(KM, LIVE, HASH)                                                                          \
     do {                                                                                                   \
         if (smem > 48 * 1024)                                                                              \
-            CU(cudaFuncSetAttribute(k_weights<KM, LIVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        k_weights<KM, LIVE><<<(n + tb - 1) / tb, tb, smem, stream>>>(h->knn, h->eta, h->nbr, h->lb_len,       \
-                                                            h->has_lb, h->g_len, gkey, T, n, h->m, (int)h->k,  \
-                                                            (int)h->kp, h->cfg.alpha, h->cfg.tau0, h->cand);   \
+            CU(cudaFuncSetAttribute(k_weights<KM, LIVE, HASH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        k_weights<KM, LIVE, HASH><<<(n + tb - 1) / tb, tb, smem, stream>>>(h->knn, h->eta, h->nbr, h->lb_len,  \
+                                                            h->has_lb, h->g_len, gkey, T, h->cand_mult, n, h->m, \
+                                                            (int)h->k, (int)h->kp, h->cfg.alpha, h->cfg.tau0, h->cand); \
     } while (0)
+#define LAUNCH_W2(KM, LIVE) do { if (hash) LAUNCH_W3(KM, LIVE, true); else LAUNCH_W3(KM, LIVE, false); } while (0)
 #define LAUNCH_W(KM) do { if (gkey) LAUNCH_W2(KM, true); else LAUNCH_W2(KM, false); } while (0)
-    if (km == 8) LAUNCH_W(8); else if (km == 16) LAUNCH_W(16); else if (km == 24) LAUNCH_W(24); else LAUNCH_W(32);
+    if (km == 8) LAUNCH_W(8); else if (km == 16) LAUNCH_W(16);
+    else if (km == 24) { if (gkey) LAUNCH_W3(24, true, false); else LAUNCH_W3(24, false, false); }
+    else { if (gkey) LAUNCH_W3(32, true, false); else LAUNCH_W3(32, false, false); }
 #undef LAUNCH_W
 #undef LAUNCH_W2
+#undef LAUNCH_W3
     CU(cudaGetLastError());
     return PACO_OK;
 }
