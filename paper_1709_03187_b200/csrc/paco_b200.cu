@@ -318,7 +318,7 @@ static paco_status setup(paco_handle* h) {
     // K1: k-NN lists, one thread per city, exact ring search over grid cells
     const int kk = (int)std::min<uint32_t>(kNearRow, n - 1);
     {
-        constexpr int T = 64;  // threads per CTA; the heaps take 12 B x kNearRow x T of shared memory
+        constexpr int T = kNearRow >= 256 ? 32 : 64;  // threads per CTA; the heaps take 12 B x kNearRow x T of shared memory
         const size_t hsm = (size_t)(sizeof(double) + sizeof(uint32_t)) * kNearRow * T;
         CU(cudaFuncSetAttribute(k_knn_cells<kNearRow, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
         k_knn_cells<kNearRow, T><<<(n + T - 1) / T, T, hsm, st>>>(h->xy, h->orig_of, h->cell_start, h->g, n, kk,
