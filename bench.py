@@ -278,7 +278,9 @@ def run_ours(args, rank, world, local):
         "cpu_baseline": cpu,
         "e2e": {"value": e2esum / e2emax, "unit": UNIT, "h2d_bytes_per_step": 16 * inst.n / cfg.iterations,
                 "d2h_bytes_per_step": (4 * inst.n + 8) / cfg.iterations,
-                "note": "paco_run: coordinates H2D, grid+k-NN build, all iterations incl. seeding, g_best D2H"},
+                "note": "paco_run: coordinates H2D, grid+k-NN build, all iterations incl. seeding, g_best D2H",
+                "wall_s": e2e_s, "device_ms": {"setup": rep.setup_ms, "construct": rep.construct_ms,
+                                               "weights_and_updates": rep.update_ms}},
         "async": {"value": a_dec / (a_ms / 1e3), "unit": UNIT, "iterations": spec["iterations"] - 1,
                   "ms": a_ms, "note": "synchronous=False (engine.hpp:213-244): one barrier-free launch for the "
                                       "config's iteration budget after seeding; weights rebuilt concurrently"},
