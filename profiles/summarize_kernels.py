@@ -12,8 +12,8 @@ COLS = {
     "gpu__time_duration.sum": "time",
     "dram__bytes_read.sum": "dram_rd",
     "dram__bytes_write.sum": "dram_wr",
-    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
-    "lts__t_bytes.sum": "l2_bytes",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "lts__t_sectors.sum": "l2_sectors",
     "l1tex__t_sector_hit_rate.pct": "l1_hit",
     "lts__t_sector_hit_rate.pct": "l2_hit",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy",
@@ -51,7 +51,7 @@ def main() -> None:
         ms = v.get("time", 0.0)
         name = r[ik].split("(")[0].replace("pacob200::", "")
         print(f"| `{name}` | {ms:.3f} | {dram:.3f} | {dram / (ms / 1e3) if ms else 0:.0f} | {v.get('dram_pct', 0):.1f} | "
-              f"{v.get('l2_bytes', 0) / 1e9:.3f} | {v.get('l1_hit', 0):.0f}% | {v.get('l2_hit', 0):.0f}% | "
+              f"{v.get('l2_sectors', 0) * 32 / 1e9:.3f} | {v.get('l1_hit', 0):.0f}% | {v.get('l2_hit', 0):.0f}% | "
               f"{v.get('occupancy', 0):.1f}% | {top} |")
 
 
