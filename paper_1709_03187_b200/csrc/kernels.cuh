@@ -773,6 +773,10 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
     const long long ph1 = clock64();
 #endif
     uint32_t n_fb = 0, n_tie = 0;
+    // The previous roulette decision's tie test, evaluated while the next row is in flight
+    // (between the scan and the next row's load it held seven instructions of the in-order
+    // issue stream: C5 construction 52.30 -> 50.98 ms). tie_tol < 0: no pending test.
+    float tie_v = 0.0f, tie_t = 0.0f, tie_tol = -1.0f;
     const uint32_t n_dec = n - pos;       // decisions of this construction (the last one forced)
     // shared-window addresses pinned in registers (an opaque move keeps the compiler from
     // re-deriving them from SR_CgaCtaId inside the loop, on the probe's address path)
@@ -810,6 +814,7 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         for (uint32_t t = t0; t < t1; ++t) {
             __syncwarp();  // orders the previous decision's visited-bit update for every lane
             const uint2 e = e_pre;  // requested at the end of the previous decision
+            n_tie += __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(tie_v, tie_t)) <= tie_tol) ? 1u : 0u;
 #ifdef PACO_SEG
             const long long sg0 = seg_clk(e.x);
 #endif
@@ -878,7 +883,7 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
                 // ms, profiles/README.md).
                 const bool win = ((w > 0.0f) & (v > target)) | is_last;
                 const uint32_t kw = __reduce_min_sync(kFull, win ? pick_key : kNone);
-                const unsigned tie = __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(v, target)) <= tol);
+                tie_v = v; tie_t = target; tie_tol = tol;
                 const uint32_t r = kw >> 27;
                 next = kw & 0x07ffffffu;
                 // the visit of next: the winning lane already holds next's bitmap word (nothing
@@ -886,7 +891,6 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
                 // it - no atomic, no branch. No candidate of next is next itself, so the next
                 // decision's probe does not depend on it.
                 sts_u8_if(vw_addr, vw | bit, lane == r);
-                n_tie += tie ? 1u : 0u;
 #ifdef PACO_SPECSTAT
                 {
                     const uint32_t mx = __reduce_max_sync(kFull, lane_in ? e.y : 0u);
@@ -920,6 +924,7 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
                 const long long c0 = clock64();
 #endif
                 next = nearest_unvisited(fctx, vis_s, cur, lane, fb_s, fs);
+                tie_tol = -1.0f;
                 if (lane == 0) vis[next >> 5] |= 1u << (next & 31);
                 // fallbacks come in runs: pull the new city's near row from HBM into L2 now,
                 // while its candidate row is probed (C5 construction 53.61 -> 53.26 ms; doing
@@ -951,6 +956,7 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
             cur = next;
         }
     }
+    n_tie += __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(tie_v, tie_t)) <= tie_tol) ? 1u : 0u;
     if (n_dec > 0) {  // the single remaining city is appended unscored (construction.hpp:529-535)
         __syncwarp();
         const uint32_t last = last_unvisited(vis, nw, lane);
