@@ -540,6 +540,7 @@ static paco_status launch_construct_async(paco_handle* h, const ConstructArgs& a
 }
 
 static paco_status check_err(paco_handle* h);
+constexpr int kWeightPassIntervalUs = 2000;  // minimum spacing of asynchronous weight passes
 
 // Asynchronous iterations (engine.hpp:213-244): one persistent launch in which every ant
 // runs `count` constructions with immediate updates, while k_weights passes rebuild the
@@ -562,10 +563,17 @@ static paco_status iterate_async(paco_handle* h, uint64_t count) {
         const cudaError_t q = cudaEventQuery(e1);
         if (q == cudaSuccess) break;
         if (q != cudaErrorNotReady) return fail(PACO_E_CUDA, cudaGetErrorString(q));
+        const auto p0 = std::chrono::steady_clock::now();
         s = launch_weights(h, h->st2, h->gkey);
         if (s != PACO_OK) return s;
         CU(cudaStreamSynchronize(h->st2));
         ++passes;
+        // Passes start at most every kWeightPassIntervalUs: a pass takes ~0.5 ms at C5, and
+        // back-to-back passes took SM time from the constructions (C5 async 2.55e9 -> 2.64e9
+        // decisions/s with 2 ms; profiles/README.md). Staleness stays about one interval.
+        while (std::chrono::steady_clock::now() - p0 < std::chrono::microseconds(kWeightPassIntervalUs)) {
+            if (cudaEventQuery(e1) != cudaErrorNotReady) break;
+        }
     }
     k_gbest_from_gkey<<<1, 1, 0, h->st>>>(h->gkey, h->gb, h->g_len);
     CU(cudaGetLastError());
