@@ -113,6 +113,9 @@ typedef struct paco_handle paco_handle;
 
 const char* paco_last_error(void);
 int paco_version(void);
+/* Device memory of destroyed handles stays cached in the device's stream-ordered pool for
+ * the next handle; this returns it to the driver (device < 0: the current device). */
+paco_status paco_release_cached_memory(int device);
 
 /* defaults of RunConfig (engine.hpp:42-59) except synchronous = 1 (deterministic per
  * seed; the reference defaults to asynchronous), plus candidates = 16 */

@@ -218,6 +218,12 @@ class Colony:
         return out, int(ln.value)
 
 
+def release_cached_memory(device: int = -1) -> None:
+    """Return the device memory of destroyed engines, kept in the device's stream-ordered
+    pool for the next engine, to the driver (paco_release_cached_memory)."""
+    N.check(N.load().paco_release_cached_memory(int(device)))
+
+
 def run(inst: Instance, cfg: RunConfig, mode: Mode = Mode.partial_aco) -> RunReport:
     """paco::run (engine.hpp:156-333) on the B200 engine."""
     lib = N.load()

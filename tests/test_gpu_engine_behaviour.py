@@ -243,3 +243,23 @@ def test_reference_rule_cases_match_paco_run(case):
                     RunConfig(ants=8, iterations=150, seed=13, rho=0.2, rule="independent"), Mode.classic_aco),
     }[case]
     check_against_reference(inst, cfg, mode, run(inst, cfg, mode))
+
+
+# ------------------------------------------------------------------ device memory pool
+
+
+def test_cached_memory_is_reused_and_released():
+    """Destroyed engines return their buffers to the device's stream-ordered pool; a new
+    engine reuses them with the same results, and paco_release_cached_memory trims it."""
+    from paper_1709_03187_b200 import Colony, release_cached_memory
+
+    inst = grid_instance(12, 9)
+    cfg = RunConfig(ants=12, iterations=6, seed=3, candidates=8)
+    lengths = []
+    for _ in range(3):
+        with Colony(inst, cfg, Mode.partial_aco) as col:
+            col.iterate(6)
+            lengths.append(col.g_best()[1])
+        release_cached_memory() if len(lengths) == 2 else None
+    assert lengths[0] == lengths[1] == lengths[2]
+    release_cached_memory(0)
