@@ -183,6 +183,10 @@ inline RunReport run(const Instance& inst, const RunConfig& cfg, Mode mode) {
 }
 
 // engine.hpp:339-344
+// Device memory of finished runs stays cached in the device's memory pool for the next
+// run; this hands it back to the driver (device < 0: the current device).
+inline void release_cached_memory(int device = -1) { check(paco_release_cached_memory(device)); }
+
 inline RunReport run_timed_baseline(const Instance& inst, RunConfig cfg, double budget_s) {
     if (budget_s <= 0.0) throw std::invalid_argument("budget must be positive");
     cfg.time_budget_s = budget_s;

@@ -58,6 +58,7 @@ int main(int argc, char** argv) {
         try { paco_b200::run(paco_b200::Instance("big", big), cfg, paco_b200::Mode::classic_aco); }
         catch (const std::invalid_argument& e) { threw = std::string(e.what()).find("n <= 5000") != std::string::npos; }
         CHECK(threw);
+        paco_b200::release_cached_memory();  // hand the pooled device memory back
     } catch (const std::runtime_error& e) {
         if (gpu) { std::fprintf(stderr, "unexpected: %s\n", e.what()); return 1; }
         std::printf("no GPU: %s\n", e.what());  // the engine has no CPU fallback
