@@ -263,3 +263,29 @@ def test_cached_memory_is_reused_and_released():
         release_cached_memory() if len(lengths) == 2 else None
     assert lengths[0] == lengths[1] == lengths[2]
     release_cached_memory(0)
+
+
+# ------------------------------------------------------------------ bench.py contract
+
+
+def test_bench_line_contract():
+    """bench.py on a small config prints one JSON line with the driver's keys."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "C2", "--steps", "2",
+                          "--warmup", "3", "--no-cpu"], capture_output=True, text=True, check=True, cwd=root).stdout
+    lines = [l for l in out.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks", "cpu_baseline"):
+        assert key in d, key
+    assert d["value"] > 0 and d["steps"] == 2 and d["warmup"] == 3 and d["n_gpus"] == 1
+    assert d["gpu_launches"] == 4 * 2
+    assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert "workload" in d["config"] and "model" not in d["config"]
