@@ -2,14 +2,14 @@
 cores) over a config's whole iteration budget, several seeds; best lengths, g_best tours
 and counters must be identical. Writes one JSON line per seed.
 
-    python profiles/parity/full_budget.py C2 1 2 3 4 5
+    python tests/parity_full_budget.py C2 1 2 3 4 5   (results: profiles/parity/*.jsonl)
 """
 import json
 import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import numpy as np  # noqa: E402
