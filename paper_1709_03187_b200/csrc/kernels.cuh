@@ -696,14 +696,15 @@ __device__ __forceinline__ uint32_t last_unvisited(const uint32_t* vis, uint32_t
 // engine.hpp:129-148 draw order). The visited bitmap (n bits) lives in shared
 // memory. The dependent chain of one decision is:
 //   candidate row of the current city (8 B per lane, one coalesced line at k = 16)
-//   -> bitmap probe -> warp inclusive scan -> ballot -> shuffle of the winner.
-// Everything else is scheduled around that chain: the next row is requested the
-// moment the winner is known, before any bookkeeping; the visited bit of the new city
-// is one lane's fire-and-forget shared-memory OR, ordered for the other lanes by the
+//   -> bitmap byte probe -> warp inclusive scan + total -> one redux.min pick whose key
+//   carries the winner's city -> the next row's load.
+// Everything else is scheduled around that chain: the visited bit of the new city is
+// the winning lane's predicated byte store, ordered for the other lanes by the
 // __syncwarp that opens the next decision; Philox draws come 128 at a time (one 4-word
-// block per lane) and the next decision's draw is fetched while its row is in flight;
-// all lane-divergent bookkeeping is predicated PTX. Preserved-segment copy, tour length
-// and the optional permutation check are warp-parallel passes around the chain.
+// block per lane) and the next decision's draw is fetched while its row is in flight,
+// as is the previous decision's tie test; all lane-divergent bookkeeping is predicated
+// PTX. Preserved-segment copy, tour length and the optional permutation check are
+// warp-parallel passes around the chain.
 //
 // KP = row stride (k rounded up to even; 0 = runtime value), STEPS = scan steps
 // (ceil(log2 k); extra steps never touch lanes < k), BUF = validation-buffer draws.
