@@ -1102,6 +1102,10 @@ __global__ void __launch_bounds__(32, 1) k_construct_async(ConstructArgs a, uint
     for (uint32_t it = 0; it < count; ++it) {
         bool partial;
         uint32_t cnt[5];
+        // gpu-scope fence per construction: the SM's L1 drops lines cached before it, so the
+        // rows this construction reads (k_weights rewrites them from other SMs) are at most
+        // one construction older than the latest pass, whatever the L1 hit rate
+        __threadfence();
         const long long len = build_one<KP, STEPS, false>(a, ant, a.iter + it, a.seeding != 0 && it == 0, smem_raw,
                                                           fctx, partial, cnt);
 #pragma unroll
@@ -1141,7 +1145,15 @@ __global__ void __launch_bounds__(32, 1) k_construct_async(ConstructArgs a, uint
                 st.has_lb[ant] = 1;
                 *(volatile int64_t*)&st.lb_len[ant] = len;
                 __threadfence();
-                atomicMin(st.gkey, ((unsigned long long)len << 16) | ant);
+                // update_g_best (colony.hpp:127-139): CAS loop with strict '<', so an equal
+                // length never displaces the incumbent
+                const unsigned long long mine = ((unsigned long long)len << 16) | ant;
+                unsigned long long cur = *(volatile unsigned long long*)st.gkey;
+                while (cur == ~0ull || (mine >> 16) < (cur >> 16)) {
+                    const unsigned long long seen = atomicCAS(st.gkey, cur, mine);
+                    if (seen == cur) break;
+                    cur = seen;
+                }
             }
             ++imps;
             __syncwarp();
@@ -1226,11 +1238,11 @@ __global__ void __launch_bounds__(1024) k_update(uint32_t first, uint32_t count,
 }
 
 // Ant::publish (colony.hpp:39-52) for the improved ants: neighbour pairs of the new
-// l_best, nbr[a][city] = (prev, next). Grid (ceil(n/256), m).
+// l_best, nbr[a][city] = (prev, next). Grid (ceil(n/256), count) covers ants first..
 __global__ void k_publish(const uint32_t* __restrict__ tours, const uint8_t* __restrict__ lb_sel,
                           const uint8_t* __restrict__ improved, uint32_t n, int current,
-                          uint2* __restrict__ nbr) {
-    const uint32_t a = blockIdx.y;
+                          uint2* __restrict__ nbr, uint32_t first = 0) {
+    const uint32_t a = first + blockIdx.y;
     if (!current && !improved[a]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
@@ -1272,6 +1284,21 @@ __global__ void __launch_bounds__(256) k_classic(const uint32_t* __restrict__ kn
 #pragma unroll
     for (int r = 0; r < KMAX; ++r)
         if (r < k) T[(size_t)i * k + r] = t[r];
+}
+
+// Readback of one tour per ant in original ids: l_best (lbest = 1), or the tour built by
+// the last iteration - the half that is not l_best unless it improved, in which case the
+// selector already flipped onto it. Grid (ceil(n/256), count) over ants first.. ; out is
+// count x n.
+__global__ void k_gather_tours(const uint32_t* __restrict__ tours, const uint8_t* __restrict__ lb_sel,
+                               const uint8_t* __restrict__ improved, const uint32_t* __restrict__ orig_of,
+                               uint32_t n, uint32_t first, int lbest, uint32_t* __restrict__ out) {
+    const uint32_t a = first + blockIdx.y;
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const uint8_t sel = lb_sel[a];
+    const uint8_t half = (lbest || improved[a]) ? sel : (uint8_t)(1 - sel);
+    out[(size_t)blockIdx.y * n + p] = orig_of[tours[((size_t)a * 2 + half) * n + p]];
 }
 
 // reference-order tour -> internal ids (host offers), and internal -> original on readback

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -41,28 +42,49 @@ paco_status fail(paco_status s, const std::string& msg) {
             return fail(PACO_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
     } while (0)
 
-// Device memory comes from the device's stream-ordered pool (cudaMallocAsync on the legacy
-// stream, then a synchronize so every stream may use it), and returns to the pool on free:
-// the pool keeps it (release threshold set to the maximum in paco_create) for the next
-// handle instead of handing it back to the driver. Measured on a fresh process after
-// another engine process: create + destroy of a C4 handle took 114-127 ms + 336-591 ms
-// through cudaMalloc/cudaFree, 11-21 ms + 3-5 ms when warm (profiles/README.md).
-// paco_release_cached_memory() trims the pool.
+// Device memory comes from the engine's own stream-ordered pool, one per device and
+// process (cudaMallocFromPoolAsync on the legacy stream, then a synchronize so every
+// stream may use it), and returns to it on free: the pool keeps it (release threshold at
+// the maximum) for the next handle instead of handing it back to the driver. The device's
+// default pool, which other cudaMallocAsync users share, is left alone. Measured on a
+// fresh process after another engine process: create + destroy of a C4 handle took
+// 114-127 ms + 336-591 ms through cudaMalloc/cudaFree, 11-21 ms + 3-5 ms when warm
+// (profiles/README.md). paco_release_cached_memory() trims the pool.
+constexpr int kMaxDevices = 64;
+cudaMemPool_t g_pool[kMaxDevices] = {};
+std::mutex g_pool_mu;
+
+cudaError_t engine_pool(int dev, cudaMemPool_t* out) {
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaError_t e = cudaMemPoolCreate(&g_pool[dev], &props);
+        if (e != cudaSuccess) { g_pool[dev] = nullptr; return e; }
+        uint64_t threshold = UINT64_MAX;
+        cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    *out = g_pool[dev];
+    return cudaSuccess;
+}
+
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
-    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), 0);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    cudaMemPool_t pool = nullptr;
+    if (e == cudaSuccess) e = engine_pool(dev, &pool);
+    if (e == cudaSuccess)
+        e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), pool, 0);
     return e != cudaSuccess ? e : cudaStreamSynchronize(0);
 }
 // callers make sure no stream still uses p
 inline void dfree(void* p) {
     if (p) cudaFreeAsync(p, 0);
-}
-inline void keep_pool(int dev) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t threshold = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
-    }
 }
 
 int kmax_for(uint32_t k) { return k <= 8 ? 8 : k <= 16 ? 16 : k <= 24 ? 24 : 32; }
@@ -137,7 +159,7 @@ paco_status paco_release_cached_memory(int device) {
     if (dev < 0) CU(cudaGetDevice(&dev));
     CU(cudaSetDevice(dev));
     cudaMemPool_t pool;
-    CU(cudaDeviceGetDefaultMemPool(&pool, dev));
+    CU(engine_pool(dev, &pool));
     CU(cudaStreamSynchronize(0));  // frees of destroyed handles complete in stream order
     CU(cudaMemPoolTrimTo(pool, 0));
     return PACO_OK;
@@ -190,6 +212,35 @@ paco_status paco_config_validate(const paco_config* c, uint32_t n, int mode) {
     if (!c->synchronous && mode != PACO_MODE_CLASSIC && c->ants > 65535)
         return fail(PACO_E_UNSUPPORTED, "asynchronous mode supports at most 65535 ants");
     return PACO_OK;
+}
+
+// Shared memory of the kernels a handle will launch, checked before anything is
+// allocated: the launch-time dynamic size plus the kernel's static shared memory.
+static size_t static_smem(const void* kern) {
+    cudaFuncAttributes fa{};
+    return cudaFuncGetAttributes(&fa, kern) == cudaSuccess ? fa.sharedSizeBytes : 0;
+}
+static size_t construct_dyn_smem(uint32_t nwords) { return kFbList * 4 + (size_t)nwords * 4 + 512 + 16; }
+static size_t construct_smem_need(uint32_t kp, uint32_t nwords, bool async_mode) {
+    const void* kerns[4];
+    int nk = 0;
+    if (kp == 16) {
+        kerns[nk++] = (const void*)k_construct<16, 4, false>; kerns[nk++] = (const void*)k_construct<16, 4, true>;
+        if (async_mode) kerns[nk++] = (const void*)k_construct_async<16, 4>;
+    } else if (kp == 20) {
+        kerns[nk++] = (const void*)k_construct<20, 5, false>; kerns[nk++] = (const void*)k_construct<20, 5, true>;
+        if (async_mode) kerns[nk++] = (const void*)k_construct_async<20, 5>;
+    } else {
+        kerns[nk++] = (const void*)k_construct<0, 5, false>; kerns[nk++] = (const void*)k_construct<0, 5, true>;
+        if (async_mode) kerns[nk++] = (const void*)k_construct_async<0, 5>;
+    }
+    size_t st = 0;
+    for (int q = 0; q < nk; ++q) st = std::max(st, static_smem(kerns[q]));
+    return construct_dyn_smem(nwords) + st;
+}
+// k_weights: ratios (8 B per ant) plus, on the hashed path, 256 threads x (32 slots + km sums)
+static size_t weights_dyn_smem(uint32_t m, int km, bool hash) {
+    return sizeof(double) * m + (hash ? (sizeof(uint32_t) * 32 + sizeof(double) * km) * 256 : 0);
 }
 
 static paco_status build_grid(paco_handle* h) {
@@ -277,17 +328,19 @@ static paco_status setup_ir(paco_handle* h) {
     std::vector<double2> xy(n);
     std::vector<uint32_t> ident(n);
     for (uint32_t i = 0; i < n; ++i) { xy[i] = make_double2(h->hx[i], h->hy[i]); ident[i] = i; }
-    CU(cudaMemcpy(h->xy, xy.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(h->orig_of, ident.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(h->int_of, ident.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+    // every copy is ordered on the handle's (non-blocking) stream and completes before
+    // setup returns: a pageable cudaMemcpy may return before its DMA lands
+    CU(cudaMemcpyAsync(h->xy, xy.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, h->st));
+    CU(cudaMemcpyAsync(h->orig_of, ident.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, h->st));
+    CU(cudaMemcpyAsync(h->int_of, ident.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, h->st));
     h->h_orig = ident;
     h->h_int = ident;
     std::vector<uint64_t> st((size_t)m * 4);
     for (uint32_t a = 0; a < m; ++a) rng_for_stream(h->cfg.seed, a, &st[(size_t)a * 4]);
     CU(dalloc(&h->rng, (size_t)m * 4));
-    CU(cudaMemcpy(h->rng, st.data(), sizeof(uint64_t) * st.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(h->rng, st.data(), sizeof(uint64_t) * st.size(), cudaMemcpyHostToDevice, h->st));
     CU(dalloc(&h->ratio, m));
-    CU(cudaMemset(h->ratio, 0, sizeof(double) * m));
+    CU(cudaMemsetAsync(h->ratio, 0, sizeof(double) * m, h->st));
     if (n <= 5000) {  // the reference keeps eta^beta in an f32 table for these sizes
         CU(dalloc(&h->eta_tab, (size_t)n * n));
         k_eta_table<<<(unsigned)(((size_t)n * n + 255) / 256), 256, 0, h->st>>>(h->xy, n, h->cfg.beta, h->eta_tab);
@@ -296,8 +349,10 @@ static paco_status setup_ir(paco_handle* h) {
     if (h->mode == PACO_MODE_CLASSIC) {  // PheromoneMatrix(n, rho, tau_max), construction.hpp:165-175
         CU(dalloc(&h->Tfull, (size_t)n * n));
         std::vector<double> init((size_t)n * n, h->cfg.tau_max);
-        CU(cudaMemcpy(h->Tfull, init.data(), sizeof(double) * init.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpyAsync(h->Tfull, init.data(), sizeof(double) * init.size(), cudaMemcpyHostToDevice, h->st));
+        CU(cudaStreamSynchronize(h->st));  // before `init` goes out of scope
     }
+    CU(cudaStreamSynchronize(h->st));
     h->setup_ms = 0.0;
     return PACO_OK;
 }
@@ -356,7 +411,10 @@ static paco_status setup(paco_handle* h) {
                                                                  (int)k, h->cfg.beta, h->knn, h->eta);
     }
     CU(cudaGetLastError());
-    if (h->mode != PACO_MODE_CLASSIC && k <= 16) {  // candidate perfect hashes for k_weights
+    int dev_optin = 0;
+    CU(cudaDeviceGetAttribute(&dev_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+    if (h->mode != PACO_MODE_CLASSIC && k <= 16 &&
+        weights_dyn_smem(h->m, kmax_for(k), true) <= (size_t)dev_optin) {  // candidate perfect hashes for k_weights
         int* dfail = nullptr;
         CU(dalloc(&h->cand_mult, n)); CU(dalloc(&dfail, 1));
         CU(cudaMemsetAsync(dfail, 0, sizeof(int), st));
@@ -375,7 +433,8 @@ static paco_status setup(paco_handle* h) {
     h->setup_ms = ms;
     cudaEventDestroy(e0); cudaEventDestroy(e1);
     h->h_orig.resize(n); h->h_int.resize(n);
-    CU(cudaMemcpy(h->h_orig.data(), h->orig_of, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(h->h_orig.data(), h->orig_of, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     for (uint32_t p = 0; p < n; ++p) h->h_int[h->h_orig[p]] = p;
     dfree(tmp); dfree(dx); dfree(dy); dfree(keys); dfree(keys2); dfree(cellm);
     return PACO_OK;
@@ -401,15 +460,20 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
     if (prop.major != 10) return fail(PACO_E_CUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
     const uint32_t nwords = (n + 31) / 32;
     const uint32_t kk = std::min<uint32_t>(cfg->candidates, n - 1), kpp = (kk + 1) & ~1u;
-    (void)kpp;
     const bool ir = cfg->rule == PACO_RULE_INDEPENDENT_ROULETTE;
-    const size_t smem_need = ir ? ir_smem_bytes(n, cfg->ants, nwords, mode) : kFbList * 4 + (size_t)nwords * 4;
+    const bool want_async = !cfg->synchronous && mode != PACO_MODE_CLASSIC;
+    const size_t optin = (size_t)prop.sharedMemPerBlockOptin;
     if (!ir && n >= (1u << 21))  // the pick packs city ids into 21 bits (implied by the bitmap bound below)
         return fail(PACO_E_UNSUPPORTED, "visited bitmap exceeds shared memory (n too large)");
-    if (smem_need > (size_t)prop.sharedMemPerBlockOptin)
-        return fail(PACO_E_UNSUPPORTED, ir ? "reference-rule per-ant state exceeds shared memory (n too large)"
-                                           : "visited bitmap exceeds shared memory (n too large)");
-    keep_pool(dev);
+    if (ir) {
+        if (ir_smem_bytes(n, cfg->ants, nwords, mode) + static_smem((const void*)k_construct_ir) > optin)
+            return fail(PACO_E_UNSUPPORTED, "reference-rule per-ant state exceeds shared memory (n too large)");
+    } else {
+        if (construct_smem_need(kpp, nwords, want_async) > optin)
+            return fail(PACO_E_UNSUPPORTED, "visited bitmap exceeds shared memory (n too large)");
+        if (mode != PACO_MODE_CLASSIC && weights_dyn_smem(cfg->ants, kmax_for(kk), false) > optin)
+            return fail(PACO_E_UNSUPPORTED, "per-ant ratios of the weight rebuild exceed shared memory (too many ants)");
+    }
     auto* h = new (std::nothrow) paco_handle();
     if (!h) return fail(PACO_E_RUNTIME, "out of host memory");
     h->ir = ir;
@@ -639,9 +703,32 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
         return iterate_async(h, count);
     }
     const uint32_t n = h->n, m = h->m;
+    // Per-iteration timing from a bounded ring of events: every kTimedRing iterations the
+    // stream is synchronized and the elapsed times folded, so a long call (the reference's
+    // default is 100000 iterations) never holds more than 4 x kTimedRing events.
+    constexpr size_t kTimedRing = 64;
     std::vector<std::pair<size_t, size_t>> marks;
     size_t e = 0;
+    double c_ms = 0, u_ms = 0;
+    auto fold = [&]() -> paco_status {
+        if (marks.empty()) return PACO_OK;
+        CU(cudaEventSynchronize(ev(h, marks.back().second)));
+        for (auto& mk : marks) {
+            float a = 0, b = 0, c = 0;
+            CU(cudaEventElapsedTime(&a, ev(h, mk.first), ev(h, mk.first + 1)));
+            CU(cudaEventElapsedTime(&b, ev(h, mk.first + 1), ev(h, mk.first + 2)));
+            CU(cudaEventElapsedTime(&c, ev(h, mk.first + 2), ev(h, mk.second)));
+            c_ms += b; u_ms += a + c;
+        }
+        marks.clear();
+        e = 0;
+        return PACO_OK;
+    };
     for (uint64_t it = 0; it < count; ++it) {
+        if (marks.size() == kTimedRing) {
+            paco_status sf = fold();
+            if (sf != PACO_OK) return sf;
+        }
         if (h->cfg.draws == PACO_DRAWS_BUFFER && !h->words_ready)
             return fail(PACO_E_INVALID, "no draw buffer set for this iteration");
         const bool seeding = h->mode != PACO_MODE_CLASSIC && h->iter == 0;
@@ -687,14 +774,8 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
         }
     }
     CU(cudaStreamSynchronize(h->st));
-    double c_ms = 0, u_ms = 0;
-    for (auto& mk : marks) {
-        float a = 0, b = 0, c = 0;
-        CU(cudaEventElapsedTime(&a, ev(h, mk.first), ev(h, mk.first + 1)));
-        CU(cudaEventElapsedTime(&b, ev(h, mk.first + 1), ev(h, mk.first + 2)));
-        CU(cudaEventElapsedTime(&c, ev(h, mk.first + 2), ev(h, mk.second)));
-        c_ms += b; u_ms += a + c;
-    }
+    paco_status sf = fold();
+    if (sf != PACO_OK) return sf;
     h->construct_ms = c_ms; h->update_ms = u_ms;
     return PACO_OK;
 }
@@ -718,29 +799,35 @@ paco_status paco_set_draws(paco_handle* h, const uint32_t* words, uint64_t strid
     return PACO_OK;
 }
 
+// Tours of every ant in original ids: a gather kernel picks each ant's half and maps the
+// ids on the device, then one copy per chunk of ants (at most 256 MB of staging).
 static paco_status read_half(paco_handle* h, bool lbest, uint32_t* tours, int64_t* lengths) {
     const uint32_t n = h->n, m = h->m;
     CU(cudaSetDevice(h->dev));
-    std::vector<uint8_t> sel(m);
-    CU(cudaMemcpy(sel.data(), h->lb_sel, m, cudaMemcpyDeviceToHost));
-    std::vector<uint32_t> buf((size_t)n);
     if (tours) {
-        for (uint32_t a = 0; a < m; ++a) {
-            // the tour built this iteration sits in the half that is not l_best, unless it
-            // improved, in which case the selector already flipped onto it
-            uint8_t half = sel[a];
-            if (!lbest) {
-                uint8_t imp = 0;
-                CU(cudaMemcpy(&imp, h->improved + a, 1, cudaMemcpyDeviceToHost));
-                half = imp ? sel[a] : (uint8_t)(1 - sel[a]);
-            }
-            CU(cudaMemcpy(buf.data(), h->tours + ((size_t)a * 2 + half) * n, sizeof(uint32_t) * n,
-                          cudaMemcpyDeviceToHost));
-            uint32_t* o = tours + (size_t)a * n;
-            for (uint32_t p = 0; p < n; ++p) o[p] = h->h_orig[buf[p]];
+        const uint32_t chunk = (uint32_t)std::max<size_t>(1, std::min<size_t>(m, (size_t)(64u << 20) / n));
+        uint32_t* stage = nullptr;
+        CU(dalloc(&stage, (size_t)chunk * n));
+        paco_status s = PACO_OK;
+        for (uint32_t a0 = 0; a0 < m && s == PACO_OK; a0 += chunk) {
+            const uint32_t c = std::min(chunk, m - a0);
+            k_gather_tours<<<dim3((n + 255) / 256, c), 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, h->orig_of,
+                                                                        n, a0, lbest ? 1 : 0, stage);
+            cudaError_t e = cudaGetLastError();
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(tours + (size_t)a0 * n, stage, sizeof(uint32_t) * n * c, cudaMemcpyDeviceToHost,
+                                    h->st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
+            if (e != cudaSuccess) s = fail(PACO_E_CUDA, std::string("tour readback: ") + cudaGetErrorString(e));
         }
+        cudaStreamSynchronize(h->st);
+        dfree(stage);
+        if (s != PACO_OK) return s;
     }
-    if (lengths) CU(cudaMemcpy(lengths, lbest ? h->lb_len : h->new_len, sizeof(int64_t) * m, cudaMemcpyDeviceToHost));
+    if (lengths) {
+        CU(cudaMemcpyAsync(lengths, lbest ? h->lb_len : h->new_len, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, h->st));
+        CU(cudaStreamSynchronize(h->st));
+    }
     return PACO_OK;
 }
 
@@ -758,16 +845,21 @@ paco_status paco_get_g_best(paco_handle* h, uint32_t* tour, int64_t* length) {
     if (!h) return fail(PACO_E_INVALID, "null handle");
     CU(cudaSetDevice(h->dev));
     GBest g{};
-    CU(cudaMemcpy(&g, h->gb, sizeof g, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&g, h->gb, sizeof g, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
     if (!g.has) { if (length) *length = -1; return PACO_OK; }
     if (length) *length = g.len;
-    if (tour) {
-        uint8_t sel = 0;
-        CU(cudaMemcpy(&sel, h->lb_sel + g.ant, 1, cudaMemcpyDeviceToHost));
-        std::vector<uint32_t> buf(h->n);
-        CU(cudaMemcpy(buf.data(), h->tours + ((size_t)g.ant * 2 + sel) * h->n, sizeof(uint32_t) * h->n,
-                      cudaMemcpyDeviceToHost));
-        for (uint32_t p = 0; p < h->n; ++p) tour[p] = h->h_orig[buf[p]];
+    if (tour) {  // g_best is the holder ant's l_best (strict-improvement invariant)
+        uint32_t* stage = nullptr;
+        CU(dalloc(&stage, h->n));
+        k_gather_tours<<<dim3((h->n + 255) / 256, 1), 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, h->orig_of,
+                                                                       h->n, (uint32_t)g.ant, 1, stage);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(tour, stage, sizeof(uint32_t) * h->n, cudaMemcpyDeviceToHost, h->st);
+        cudaStreamSynchronize(h->st);
+        dfree(stage);
+        if (e != cudaSuccess) return fail(PACO_E_CUDA, std::string("g_best readback: ") + cudaGetErrorString(e));
     }
     return PACO_OK;
 }
@@ -776,7 +868,8 @@ paco_status paco_get_counters(paco_handle* h, paco_counters* c) {
     if (!h || !c) return fail(PACO_E_INVALID, "null argument");
     CU(cudaSetDevice(h->dev));
     unsigned long long v[16];
-    CU(cudaMemcpy(v, h->counters, sizeof v, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(v, h->counters, sizeof v, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
     c->decisions = v[0]; c->fallbacks = v[1]; c->ties = v[2]; c->forced = v[3];
     c->full_builds = v[4]; c->partial_builds = v[5]; c->iterations = h->iter; c->improvements = v[7];
     c->comparisons = h->ir ? v[8] : v[0];
@@ -787,8 +880,9 @@ paco_status paco_get_counters(paco_handle* h, paco_counters* c) {
 paco_status paco_get_build_flags(paco_handle* h, uint8_t* partial, uint8_t* improved) {
     if (!h) return fail(PACO_E_INVALID, "null handle");
     CU(cudaSetDevice(h->dev));
-    if (partial) CU(cudaMemcpy(partial, h->partial, h->m, cudaMemcpyDeviceToHost));
-    if (improved) CU(cudaMemcpy(improved, h->improved, h->m, cudaMemcpyDeviceToHost));
+    if (partial) CU(cudaMemcpyAsync(partial, h->partial, h->m, cudaMemcpyDeviceToHost, h->st));
+    if (improved) CU(cudaMemcpyAsync(improved, h->improved, h->m, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
     return PACO_OK;
 }
 
@@ -800,8 +894,9 @@ paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, u
     if (k_out) *k_out = k;
     std::vector<uint2> c((size_t)n * h->kp);
     std::vector<uint32_t> kn((size_t)n * kNearRow);
-    CU(cudaMemcpy(kn.data(), h->knn, sizeof(uint32_t) * kn.size(), cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(c.data(), h->cand, sizeof(uint2) * c.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(kn.data(), h->knn, sizeof(uint32_t) * kn.size(), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(c.data(), h->cand, sizeof(uint2) * c.size(), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
     for (uint32_t o = 0; o < n; ++o) {
         const uint32_t i = h->h_int[o];
         for (uint32_t r = 0; r < k; ++r) {
@@ -853,21 +948,23 @@ paco_status paco_offer_tour(paco_handle* h, uint32_t ant, const uint32_t* order,
     CU(cudaSetDevice(h->dev));
     std::vector<uint32_t> in(n);
     for (uint32_t i = 0; i < n; ++i) in[i] = h->h_int[order[i]];
+    // every transfer is ordered on the handle's stream (pageable copies may return before
+    // their DMA lands) and `in` / `L` outlive them (synchronize below)
     uint8_t sel = 0;
-    CU(cudaMemcpy(&sel, h->lb_sel + ant, 1, cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(h->tours + ((size_t)ant * 2 + (1 - sel)) * n, in.data(), sizeof(uint32_t) * n,
-                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(&sel, h->lb_sel + ant, 1, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    CU(cudaMemcpyAsync(h->tours + ((size_t)ant * 2 + (1 - sel)) * n, in.data(), sizeof(uint32_t) * n,
+                       cudaMemcpyHostToDevice, h->st));
     const int64_t L = host_length(h, order);
-    CU(cudaMemcpy(h->new_len + ant, &L, sizeof L, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(h->new_len + ant, &L, sizeof L, cudaMemcpyHostToDevice, h->st));
     k_update<<<1, 32, 0, h->st>>>(ant, 1, h->new_len, h->lb_len, h->has_lb, h->lb_sel, h->improved, h->gb,
                                   h->g_len, h->counters);
-    dim3 grid((n + 255) / 256, h->m);
-    k_publish<<<grid, 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, n, 0, h->nbr);
+    // publish only this ant's slice (grid.y = 1 at ant offset `ant`)
+    k_publish<<<dim3((n + 255) / 256, 1), 256, 0, h->st>>>(h->tours, h->lb_sel, h->improved, n, 0, h->nbr, ant);
     CU(cudaGetLastError());
-    CU(cudaStreamSynchronize(h->st));
     uint8_t imp = 0;
-    CU(cudaMemcpy(&imp, h->improved + ant, 1, cudaMemcpyDeviceToHost));
-    // only `ant` may publish: clear the others' flags that k_update did not touch
+    CU(cudaMemcpyAsync(&imp, h->improved + ant, 1, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
     if (improved) *improved = imp;
     return PACO_OK;
 }
@@ -883,18 +980,20 @@ paco_status paco_construct_at(paco_handle* h, uint32_t ant, uint32_t start_pos, 
     if (h->ir) return fail(PACO_E_UNSUPPORTED, "construct_at is defined for the candidate-list rule");
     CU(cudaSetDevice(h->dev));
     uint8_t has = 0;
-    CU(cudaMemcpy(&has, h->has_lb + ant, 1, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&has, h->has_lb + ant, 1, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
     if (!has) return fail(PACO_E_INVALID, "ant has no l_best");
     uint32_t* dw = nullptr;
     CU(dalloc(&dw, nwords));
-    CU(cudaMemcpy(dw, words, sizeof(uint32_t) * nwords, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(dw, words, sizeof(uint32_t) * nwords, cudaMemcpyHostToDevice, h->st));
     paco_status s = launch_weights(h);
     if (s != PACO_OK) { dfree(dw); return s; }
     ConstructArgs a = construct_args(h, false);
     a.words = dw; a.stride = nwords; a.force = 1; a.force_ant = ant; a.force_start_pos = start_pos;
     a.force_m_mod = m_mod; a.validate = 1;
     int64_t saved_len = 0;
-    CU(cudaMemcpy(&saved_len, h->new_len + ant, sizeof saved_len, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&saved_len, h->new_len + ant, sizeof saved_len, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
     CU(cudaMemsetAsync(h->err, 0, sizeof(int), h->st));
     s = launch_construct(h, a, 1);
     if (s != PACO_OK) { dfree(dw); return s; }
@@ -903,13 +1002,15 @@ paco_status paco_construct_at(paco_handle* h, uint32_t ant, uint32_t start_pos, 
     s = check_err(h);
     if (s != PACO_OK) return s;
     uint8_t sel = 0;
-    CU(cudaMemcpy(&sel, h->lb_sel + ant, 1, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&sel, h->lb_sel + ant, 1, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
     std::vector<uint32_t> buf(n);
-    CU(cudaMemcpy(buf.data(), h->tours + ((size_t)ant * 2 + (1 - sel)) * n, sizeof(uint32_t) * n,
-                  cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(buf.data(), h->tours + ((size_t)ant * 2 + (1 - sel)) * n, sizeof(uint32_t) * n,
+                       cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(out_length, h->new_len + ant, sizeof(int64_t), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(h->new_len + ant, &saved_len, sizeof saved_len, cudaMemcpyHostToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));  // saved_len outlives its copy
     for (uint32_t p = 0; p < n; ++p) out_order[p] = h->h_orig[buf[p]];
-    CU(cudaMemcpy(out_length, h->new_len + ant, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(h->new_len + ant, &saved_len, sizeof saved_len, cudaMemcpyHostToDevice));
     return PACO_OK;
 }
 
@@ -944,7 +1045,8 @@ paco_status paco_run_traced(const double* xs, const double* ys, uint32_t n, cons
         const double t = since();
         if (s == PACO_OK && sampling && t >= next_t && ns + 1 < cap) {
             GBest g{};
-            if (cudaMemcpy(&g, h->gb, sizeof g, cudaMemcpyDeviceToHost) == cudaSuccess && g.has)
+            if (cudaMemcpyAsync(&g, h->gb, sizeof g, cudaMemcpyDeviceToHost, h->st) == cudaSuccess &&
+                cudaStreamSynchronize(h->st) == cudaSuccess && g.has)
                 samples[ns++] = paco_sample{t, g.len, done};
             while (next_t <= t) next_t += interval;
         }
