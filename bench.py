@@ -118,19 +118,37 @@ def cpu_reference_sample(spec, inst, seconds, threads):
 
 
 def cpu_port_sample(spec, inst, threads, ants):
-    """O2 (the restatement of the north-star rule) on the host cores: one seeding +
-    one partial iteration of a reduced colony on the same instance."""
+    """O2 (oracle/o2.c: the same north-star rule restated in C, pthreads over ants) on the
+    host cores: the seeding iteration plus two partial iterations of a colony of `ants`
+    ants on the same instance (the like-for-like CPU rate of the rule the GPU runs)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
 
-    o = oracle.O2(inst.xs, inst.ys, m=ants, k=spec["k"], seed=3, threads=threads) if inst.n <= 20000 else None
-    if o is None:
-        return None
+    o = oracle.O2(inst.xs, inst.ys, m=ants, k=spec["k"], seed=3, threads=threads)
     t0 = time.perf_counter()
-    o.iterate()
-    o.iterate()
+    for _ in range(3):
+        o.iterate()
     dt = time.perf_counter() - t0
-    return o.counters()["decisions"] / dt
+    return o.counters()["decisions"] / dt, o.counters()["decisions"], dt
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 def run_reference_arm(args, rank, world):
@@ -221,10 +239,12 @@ def run_ours(args, rank, world, local):
     a_dec = acol.counters()["decisions"] - a0["decisions"]
     acol.close()
 
-    # end to end through the public C-ABI call: host coordinates in, g_best tour out
+    # end to end through the public C-ABI call (paco_run, the drop-in for paco::run):
+    # host coordinates in, the config's whole iteration budget, g_best tour out
+    ecfg = RunConfig(**{**cfg.__dict__, "iterations": spec["iterations"]})
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rep = paco_run(inst, cfg, Mode.partial_aco)
+    rep = paco_run(inst, ecfg, Mode.partial_aco)
     e2e_s = time.perf_counter() - t0
     e2e_dec = rep.counters["decisions"]
 
@@ -237,28 +257,39 @@ def run_ours(args, rank, world, local):
     c_ms_avg = sum(construct_ms) / len(construct_ms)
     bytes_per_launch = b_dec(k) * (decisions / args.steps)
     achieved = bytes_per_launch / (c_ms_avg / 1e3) / 1e9
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get("k_construct", {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
-    cpu = None
+    # traffic: DRAM bytes per launch from the committed ncu --set full capture of THIS config
+    # (profiles/ncu_summary.json, keyed by config); null when the config has no capture
+    ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")).get("k_construct", {}).get(args.config, {})
+    traffic = ncu.get("dram_bytes_per_launch")
+    l2_traffic = ncu.get("l2_bytes_per_launch")
+    l2peak = load_json(os.path.join(ROOT, "profiles", "l2_peak.json"))
+    l2_gbs = l2peak.get("l2_read_gbs")
+    dec_per_iter = decisions / args.steps
+    cpu = port = None
+    host = {"cpu_model": cpu_model(), "threads": os.cpu_count() or 1}
     if world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         try:
             rate, r = cpu_reference_sample(spec, inst, args.cpu_seconds, threads)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"{r['decisions']} paco::select_next calls (unmodified reference, IR rule) on the "
-                             f"{args.config} instance, {args.cpu_seconds:.0f}s on {threads} threads"}
+                             f"{args.config} instance, {args.cpu_seconds:.0f}s on {threads} threads",
+                   "iteration_s_extrapolated": dec_per_iter / rate if rate else None}
         except Exception as e:  # the reference harness is test infrastructure; report, do not fail
             cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "sample": f"unavailable: {e}"}
+        try:
+            ants = min(spec["m"], 4 * threads)
+            prate, pdec, pdt = cpu_port_sample(spec, inst, threads, ants)
+            port = {"value": prate, "unit": UNIT, "cores": threads, "kind": "port",
+                    "sample": f"O2 (the north-star rule restated in C, oracle/o2.c) on the {args.config} instance: "
+                              f"seeding + 2 partial iterations of a {ants}-ant colony, {pdec} decisions in "
+                              f"{pdt:.1f}s on {threads} threads",
+                    "iteration_s_extrapolated": dec_per_iter / prate if prate else None,
+                    "gpu_speedup_same_rule": value / prate if prate else None}
+        except Exception as e:
+            port = {"value": None, "unit": UNIT, "cores": threads, "kind": "port", "sample": f"unavailable: {e}"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -274,11 +305,28 @@ def run_ours(args, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_construct",
                      "bytes_per_decision": b_dec(k), "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks
-                     else "fallback 6650 GB/s (B200_PROFILING.md)"},
+                     else "fallback 6650 GB/s (B200_PROFILING.md)",
+                     "traffic_source": (f"profiles/ncu_summary.json k_construct.{args.config} (ncu --set full, "
+                                        "dram__bytes_read+write per launch)") if traffic is not None else
+                                       f"no ncu capture committed for {args.config}",
+                     "l2": {"achieved": achieved, "peak": l2_gbs, "unit": "GB/s",
+                            "frac": achieved / l2_gbs if l2_gbs else None,
+                            "traffic": l2_traffic,
+                            "peak_source": "profiles/l2_peak.json (ub_l2_bw.cu, L2-resident read bandwidth "
+                                           "measured on a B200)" if l2_gbs else None,
+                            "note": "the per-decision tables (candidate rows, 25.6 MB at C5) are L1/L2-resident: "
+                                    "same algorithmic bytes against the L2 bandwidth"}},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2esum / e2emax, "unit": UNIT, "h2d_bytes_per_step": 16 * inst.n / cfg.iterations,
-                "d2h_bytes_per_step": (4 * inst.n + 8) / cfg.iterations,
-                "note": "paco_run: coordinates H2D, grid+k-NN build, all iterations incl. seeding, g_best D2H",
+        "cpu_baseline_port": port,
+        "host": {**host, "gpu_iteration_ms": tmax / args.steps,
+                 "reference_iteration_s_extrapolated": (cpu or {}).get("iteration_s_extrapolated"),
+                 "port_iteration_s_extrapolated": (port or {}).get("iteration_s_extrapolated"),
+                 "note": "host-core time for one iteration of this config = decisions per GPU iteration / "
+                         "host rate (the reference's own rule for `reference`, the same rule for `port`)"},
+        "e2e": {"value": e2esum / e2emax, "unit": UNIT, "h2d_bytes_per_step": 16 * inst.n / ecfg.iterations,
+                "d2h_bytes_per_step": (4 * inst.n + 8) / ecfg.iterations, "iterations": ecfg.iterations,
+                "note": "paco_run: coordinates H2D, grid+k-NN build, the config's whole iteration budget incl. "
+                        "seeding, g_best D2H",
                 "wall_s": e2e_s, "device_ms": {"setup": rep.setup_ms, "construct": rep.construct_ms,
                                                "weights_and_updates": rep.update_ms}},
         "async": {"value": a_dec / (a_ms / 1e3), "unit": UNIT, "iterations": spec["iterations"] - 1,

@@ -87,6 +87,7 @@ typedef struct paco_counters {
     uint64_t improvements;   /* successful update_l_best calls */
     uint64_t comparisons;    /* candidate scores evaluated (IR rule: the reference's comparison count) */
     uint64_t two_opts;       /* constructions that ran 2-opt (maybe_two_opt, two_opt.hpp:71-76) */
+    uint64_t two_opt_moves;  /* accepted 2-opt moves (synchronous engine) */
 } paco_counters;
 
 /* RunReport, engine.hpp:84-92 (+ counters and device-time breakdown) */

@@ -48,7 +48,7 @@ class Config(ctypes.Structure):
 class Counters(ctypes.Structure):
     _fields_ = [(name, c_uint64) for name in (
         "decisions", "fallbacks", "ties", "forced", "full_builds", "partial_builds", "iterations",
-        "improvements", "comparisons", "two_opts")]
+        "improvements", "comparisons", "two_opts", "two_opt_moves")]
 
     def as_dict(self) -> dict:
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

@@ -370,6 +370,7 @@ struct ConstructArgs {
     // explicit construct_partial_at (tests): ant = force_ant, params given
     double two_opt_prob;       // maybe_two_opt (two_opt.hpp:71-76), draw slot 3
     uint32_t two_opt_window;
+    uint8_t* two_opt_flag;     // non-null: record the draw for k_two_opt instead of searching inline
     int force;
     uint32_t force_ant, force_start_pos, force_m_mod;
 };
@@ -994,10 +995,16 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
 #ifdef PACO_PHASES
     const long long ph2 = clock64();
 #endif
-    // maybe_two_opt (two_opt.hpp:71-76): draw slot 3
+    // maybe_two_opt (two_opt.hpp:71-76): draw slot 3. The synchronous engine defers the
+    // search to k_two_opt (a whole CTA per tour, after this kernel; the length computed
+    // below is then corrected by the search's delta); the asynchronous one runs it here.
     uint32_t n_2opt = 0;
     if (!a.force && a.two_opt_prob > 0.0 && u01_f64(word(3)) < a.two_opt_prob) {
-        two_opt_warp(out, n, a.two_opt_window, a.xy, lane);
+        if (a.two_opt_flag) {
+            if (lane == 0) a.two_opt_flag[ant] = 1;
+        } else {
+            two_opt_exact<false>(out, n, a.two_opt_window, a.xy, nullptr, nullptr, nullptr, nullptr);
+        }
         n_2opt = 1;
     }
     // tour length (instance.hpp:120-127), int64, warp-parallel over positions
@@ -1299,6 +1306,29 @@ __global__ void k_gather_tours(const uint32_t* __restrict__ tours, const uint8_t
     const uint8_t sel = lb_sel[a];
     const uint8_t half = (lbest || improved[a]) ? sel : (uint8_t)(1 - sel);
     out[(size_t)blockIdx.y * n + p] = orig_of[tours[((size_t)a * 2 + half) * n + p]];
+}
+
+// maybe_two_opt's search for the synchronous engine (two_opt.hpp:28-67): one CTA per
+// flagged tour (the new tour in the ant's non-l_best half, before k_update), the CTA-wide
+// exact first-improvement search of two_opt_exact, the length corrected by its delta.
+// CTAs loop over the ants; `edges` holds one n-entry edge cache per CTA.
+__global__ void __launch_bounds__(512, 1) k_two_opt(uint32_t* __restrict__ tours, const uint8_t* __restrict__ lb_sel,
+                                                  uint8_t* __restrict__ flag, int64_t* __restrict__ new_len,
+                                                  uint32_t n, uint32_t m, uint32_t window,
+                                                  const double2* __restrict__ xy, int32_t* __restrict__ edges,
+                                                  double2* __restrict__ txy, unsigned long long* __restrict__ moves) {
+    __shared__ unsigned long long s_key[33];
+    int32_t* e = edges + (size_t)blockIdx.x * n;
+    double2* tx = txy + (size_t)blockIdx.x * n;
+    for (uint32_t a = blockIdx.x; a < m; a += gridDim.x) {
+        if (!flag[a]) continue;  // CTA-uniform
+        uint32_t* o = tours + ((size_t)a * 2 + (1 - lb_sel[a])) * n;
+        uint32_t mv = 0;
+        const long long d = two_opt_block(o, n, window, xy, e, tx, s_key, &mv);
+        __syncthreads();
+        if (threadIdx.x == 0) { new_len[a] += d; flag[a] = 0; atomicAdd(moves, (unsigned long long)mv); }
+        __syncthreads();
+    }
 }
 
 // reference-order tour -> internal ids (host offers), and internal -> original on readback

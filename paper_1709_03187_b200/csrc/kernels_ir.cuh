@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
         for (int q = 0; q < 4; ++q) a.rng[(size_t)ant * 4 + q] = s[q];
     }
     __syncwarp();
-    if (do2) two_opt_warp(out, n, a.two_opt_window, a.xy, lane);
+    if (do2) two_opt_exact<false>(out, n, a.two_opt_window, a.xy, nullptr, nullptr, nullptr, nullptr);
     const long long len = warp_tour_length(out, n, a.xy, lane);
     if (lane == 0) {
         a.new_len[ant] = len;

@@ -105,6 +105,11 @@ struct paco_handle {
     double2* xy = nullptr;
     uint32_t *orig_of = nullptr, *int_of = nullptr, *cell_start = nullptr, *sb_start = nullptr;
     uint32_t* knn = nullptr;
+    // synchronous 2-opt (k_two_opt): per-ant request flags and one edge cache per CTA
+    uint8_t* two_opt_flag = nullptr;
+    int32_t* two_opt_edges = nullptr;
+    double2* two_opt_txy = nullptr;
+    uint32_t two_opt_ctas = 0;
     float* eta = nullptr;
     uint2* cand = nullptr;
     uint32_t* tours = nullptr;
@@ -140,7 +145,7 @@ struct paco_handle {
         if (st) cudaStreamSynchronize(st);  // nothing may still use the buffers returned below
         if (st2) cudaStreamSynchronize(st2);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
-                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words,
+                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words, two_opt_flag, two_opt_edges, two_opt_txy,
                         scratch_u32, scratch_u64, rng, ratio, Tfull, eta_tab, cand_mult};
         for (void* p : ptrs) dfree(p);
         for (auto e : evpool) cudaEventDestroy(e);
@@ -299,6 +304,13 @@ static paco_status alloc_colony(paco_handle* h) {
     CU(cudaMemsetAsync(h->counters, 0, 16 * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(h->err, 0, sizeof(int), st));
     if (h->mode == PACO_MODE_CLASSIC) CU(dalloc(&h->cur_nbr, (size_t)m * n));
+    if (!h->ir && !h->async_mode && h->cfg.two_opt_prob > 0.0) {
+        h->two_opt_ctas = std::min<uint32_t>(m, 64);
+        CU(dalloc(&h->two_opt_flag, m));
+        CU(dalloc(&h->two_opt_edges, (size_t)h->two_opt_ctas * n));
+        CU(dalloc(&h->two_opt_txy, (size_t)h->two_opt_ctas * n));
+        CU(cudaMemsetAsync(h->two_opt_flag, 0, m, st));
+    }
     CU(cudaStreamSynchronize(st));
     return PACO_OK;
 }
@@ -592,6 +604,7 @@ static ConstructArgs construct_args(paco_handle* h, bool seeding) {
     a.validate = h->cfg.validate_tours ? 1 : 0;
     a.err = h->err;
     a.two_opt_prob = h->cfg.two_opt_prob; a.two_opt_window = h->cfg.two_opt_window;
+    a.two_opt_flag = h->async_mode ? nullptr : h->two_opt_flag;  // async: inline search
     return a;
 }
 
@@ -739,6 +752,12 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
         CU(cudaEventRecord(ev(h, e1), h->st));
         s = h->ir ? launch_construct_ir(h, seeding) : launch_construct(h, construct_args(h, seeding), m);
         if (s != PACO_OK) return s;
+        if (h->two_opt_flag) {  // maybe_two_opt's searches, one CTA per flagged tour (k_two_opt)
+            k_two_opt<<<h->two_opt_ctas, 512, 0, h->st>>>(h->tours, h->lb_sel, h->two_opt_flag, h->new_len, n, m,
+                                                          h->cfg.two_opt_window, h->xy, h->two_opt_edges,
+                                                          h->two_opt_txy, h->counters + 10);
+            CU(cudaGetLastError());
+        }
         CU(cudaEventRecord(ev(h, e2), h->st));
         if (h->ir && h->mode == PACO_MODE_CLASSIC) {
             // full-matrix evaporate + deposit (construction.hpp:187-207), engine.hpp:253-259
@@ -874,6 +893,7 @@ paco_status paco_get_counters(paco_handle* h, paco_counters* c) {
     c->full_builds = v[4]; c->partial_builds = v[5]; c->iterations = h->iter; c->improvements = v[7];
     c->comparisons = h->ir ? v[8] : v[0];
     c->two_opts = v[9];
+    c->two_opt_moves = v[10];
     return PACO_OK;
 }
 

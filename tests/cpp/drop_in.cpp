@@ -3,6 +3,7 @@
 // Usage: drop_in [expect-gpu 0|1]
 #include <cstdio>
 #include <cstdlib>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 
@@ -19,6 +20,28 @@ int main(int argc, char** argv) {
     try { bad.validate(); } catch (const std::invalid_argument& e) { threw = std::string(e.what()) == "ants must be >= 1"; }
     CHECK(threw);
     CHECK(paco_b200::mode_from_name("partial") == paco_b200::Mode::partial_aco);
+    CHECK(!paco_b200::RunConfig{}.synchronous);  // engine.hpp:58 default: the asynchronous engine
+    // parse_tsplib / parse_tsplib_file (instance.hpp:164-249): rules and messages
+    {
+        std::istringstream ok("NAME : tri\nTYPE : TSP\nDIMENSION : 3\nEDGE_WEIGHT_TYPE : EUC_2D\n"
+                              "NODE_COORD_SECTION\n1 0 0\n2 3 0\n3 3 4\nEOF\n");
+        const auto tri = paco_b200::parse_tsplib(ok);
+        CHECK(tri.name() == "tri" && tri.n() == 3 && tri.dist(0, 2) == 5);
+        std::istringstream geo("NAME : x\nDIMENSION : 3\nEDGE_WEIGHT_TYPE : GEO\n");
+        threw = false;
+        try { paco_b200::parse_tsplib(geo); }
+        catch (const paco_b200::ParseError& e) { threw = std::string(e.what()) == "line 3: unsupported EDGE_WEIGHT_TYPE: 'GEO' (only EUC_2D)"; }
+        CHECK(threw);
+        std::istringstream shortf("DIMENSION : 4\nEDGE_WEIGHT_TYPE : EUC_2D\nNODE_COORD_SECTION\n1 0 0\n2 1 1\n3 2 2\nEOF\n");
+        threw = false;
+        try { paco_b200::parse_tsplib(shortf); }
+        catch (const paco_b200::ParseError& e) { threw = std::string(e.what()) == "line 7: DIMENSION is 4 but 3 coordinate lines were read"; }
+        CHECK(threw);
+        threw = false;
+        try { paco_b200::parse_tsplib_file("/nonexistent/x.tsp"); }
+        catch (const std::runtime_error& e) { threw = std::string(e.what()) == "cannot open instance file: /nonexistent/x.tsp"; }
+        CHECK(threw);
+    }
 
     // grid442 (26 x 17 lattice, spacing 10, optimum 4420)
     std::vector<std::pair<double, double>> pts;
@@ -26,6 +49,7 @@ int main(int argc, char** argv) {
     paco_b200::Instance inst("grid442", pts, 4420);
     paco_b200::RunConfig cfg;
     cfg.ants = 16; cfg.iterations = 50; cfg.alpha = 1.0; cfg.beta = 2.0; cfg.candidates = 12; cfg.seed = 3;
+    cfg.synchronous = true;
     try {
         const auto rep = paco_b200::run(inst, cfg, paco_b200::Mode::partial_aco);
         CHECK(gpu);

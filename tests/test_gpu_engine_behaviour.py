@@ -289,3 +289,6 @@ def test_bench_line_contract():
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert "workload" in d["config"] and "model" not in d["config"]
+    # traffic is the committed ncu capture of THIS config, or null (never another config's)
+    assert "C2" in d["roofline"]["traffic_source"]
+    assert d["e2e"]["iterations"] == 200 and "host" in d

@@ -142,6 +142,16 @@ def test_two_opt_after_construction(p2, w2):
     assert col.counters()["two_opts"] == ref.counters()["two_opts"] > 0
 
 
+@pytest.mark.parametrize("n,w2", [(3000, 100), (1500, 0)])
+def test_two_opt_exact_sequence_on_longer_tours(n, w2):
+    """The synchronous engine's k_two_opt (CTA-wide scan, restart at i - W after a move, squared-
+    distance filter) ends every search on O2's tour, and O2 restates two_opt.hpp:28-67 literally
+    (restart from i = 0 after every move): the same move sequence, hence the same local optimum."""
+    inst = make_config_instance("C2", n=n)
+    col, ref = lockstep(inst, 4, ants=16, candidates=16, two_opt_prob=0.3, two_opt_window=w2, seed=9)
+    assert col.counters()["two_opts"] == ref.counters()["two_opts"] > 0
+
+
 def test_validation_buffer_draws():
     rng = np.random.default_rng(5)
 
@@ -388,3 +398,20 @@ def test_cpp_drop_in_on_gpu(tmp_path):
     out = subprocess.run([exe, "1"], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr + out.stdout
     assert "drop_in ok" in out.stdout
+
+
+def test_cpp_reference_types_drop_in_on_gpu():
+    """The prebuilt tests/cpp/_build/ref_drop_in (compiled against the unmodified reference headers
+    by __graft_entry__.build()): paco_b200::run on paco::Instance / paco::RunConfig / paco::Mode
+    returns a paco::RunReport; with the reference's rule and synchronous iterations it equals
+    paco::run, compiled into the same binary, bit for bit."""
+    import os
+    import subprocess
+    from test_host import REF_DROP_IN
+    from paper_1709_03187_b200 import _native
+    _native.load()
+    if not os.path.exists(REF_DROP_IN):
+        pytest.skip("ref_drop_in was not built (needs the reference headers at build time)")
+    out = subprocess.run([REF_DROP_IN, "1"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert "ref_drop_in ok" in out.stdout

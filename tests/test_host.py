@@ -214,6 +214,36 @@ def build_drop_in(tmp_dir):
     return exe
 
 
+REF_INCLUDE = "/root/reference/proj/include"
+REF_DROP_IN = os.path.join(ROOT, "tests", "cpp", "_build", "ref_drop_in")
+
+
+def build_ref_drop_in(out_path=REF_DROP_IN):
+    """tests/cpp/ref_drop_in.cpp against the unmodified reference headers (needs /root/reference;
+    __graft_entry__.build() runs this in the build container, the binary travels with the repo)."""
+    os.makedirs(os.path.dirname(out_path), exist_ok=True)
+    lib = os.path.dirname(N.LIB_PATH)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-pthread", "-I", REF_INCLUDE, "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "ref_drop_in.cpp"), "-L", lib, "-lpaco_b200",
+                    f"-Wl,-rpath,{lib}", "-o", out_path], check=True)
+    return out_path
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INCLUDE), reason="reference headers not present (GPU box)")
+def test_cpp_drop_in_on_reference_types_compiles_and_fails_loudly_without_gpu(native, tmp_path):
+    """paco_b200::run(const paco::Instance&, const paco::RunConfig&, paco::Mode) -> paco::RunReport
+    compiles in one translation unit with the unmodified reference headers (SURVEY §8(b));
+    the reference's validation errors come through unchanged and, without a GPU, the run
+    throws instead of falling back to the CPU."""
+    import torch
+    exe = build_ref_drop_in(str(tmp_path / "ref_drop_in"))
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by tests/test_gpu_parity.py::test_cpp_reference_types_drop_in_on_gpu")
+    out = subprocess.run([exe, "0"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert "no GPU" in out.stdout
+
+
 def test_cpp_drop_in_header_compiles_and_fails_loudly_without_gpu(native, tmp_path):
     """include/paco_b200/paco.hpp is the reference's C++ calling convention over the C ABI."""
     import torch
