@@ -80,7 +80,7 @@ typedef struct paco_counters {
     uint64_t decisions;      /* cities placed by the selection rule (incl. forced last city) */
     uint64_t fallbacks;      /* decisions where every candidate was visited */
     uint64_t ties;           /* roulette boundary ties |S_r - u*S| <= 1e-6*S (logged, not resolved) */
-    uint64_t forced;         /* single-candidate appends (construction.hpp:529-535) */
+    uint64_t forced;         /* single-candidate appends (construction.hpp:342-348) */
     uint64_t full_builds;
     uint64_t partial_builds;
     uint64_t iterations;

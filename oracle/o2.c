@@ -288,7 +288,7 @@ static int complete_tour(const o2_state* s, uint32_t ant, uint32_t* order, uint3
         uint32_t next;
         c->decisions++;
         if (remaining == 1) {
-            /* final city is forced, no score evaluated (construction.hpp:529-535) */
+            /* final city is forced, no score evaluated (construction.hpp:342-348) */
             next = UINT32_MAX;
             for (uint32_t j = 0; j < n; ++j) if (!vis[j]) { next = j; break; }
             c->forced++;

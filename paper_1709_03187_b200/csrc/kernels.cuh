@@ -181,33 +181,43 @@ __global__ void __launch_bounds__(T) k_knn_cells(const double2* __restrict__ xy,
 
 // ============================================================ K5: weight table
 // Per-city perfect hash of the candidate list (setup, once per instance): the multiplier
-// M_i maps the k <= 16 candidates of city i to distinct slots (c * M_i) >> 27 of 32, so
+// M_i maps the k candidates of city i to distinct slots (c * M_i) >> (32 - B) of 2^B, so
 // k_weights finds the candidate index of a neighbour with one shared-memory lookup
-// instead of k comparisons. Trial multipliers are odd SplitMix values of (i, trial);
-// success probability per trial is 1.04% at k = 16 (about 96 trials), 2^14 trials are
-// allowed; a city without one sets *fail and k_weights keeps the comparison loop.
-constexpr int kHashSlotBits = 5;
-__device__ __forceinline__ uint32_t cand_slot(uint32_t c, uint32_t M) { return (c * M) >> (32 - kHashSlotBits); }
+// instead of k comparisons. B = hash_slot_bits(k): 32 slots for k <= 16 (success 1.04%
+// per trial at k = 16), 64 for k <= 24 (0.8% at k = 24, 5.1% at k = 20), 128 for k <= 32
+// (1.5% at k = 32). Trial multipliers are odd SplitMix values of (i, trial), 2^14 trials
+// are allowed; a city without one sets *fail and k_weights keeps the comparison loop.
+__host__ __device__ constexpr int hash_slot_bits(int kmax) { return kmax <= 16 ? 5 : kmax <= 24 ? 6 : 7; }
+template <int B>
+__device__ __forceinline__ uint32_t cand_slot(uint32_t c, uint32_t M) { return (c * M) >> (32 - B); }
+template <int KMAX>
 __global__ void k_cand_hash(const uint32_t* __restrict__ knn32, uint32_t n, int k, uint32_t* __restrict__ mult,
                             int* __restrict__ fail) {
+    constexpr int B = hash_slot_bits(KMAX), W = (1 << B) / 32;
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    uint32_t c[16];
+    uint32_t c[KMAX];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) c[r] = r < k ? knn32[(size_t)i * kNearRow + r] : 0u;
+    for (int r = 0; r < KMAX; ++r) c[r] = r < k ? knn32[(size_t)i * kNearRow + r] : 0u;
     for (uint32_t t = 0; t < (1u << 14); ++t) {
         unsigned long long z = ((unsigned long long)i << 20 | t) + 0x9e3779b97f4a7c15ull;
         z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
         z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
         const uint32_t M = (uint32_t)(z ^ (z >> 31)) | 1u;
-        uint32_t used = 0;
+        uint32_t used[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) used[w] = 0;
         bool ok = true;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
+        for (int r = 0; r < KMAX; ++r) {
             if (r < k) {
-                const uint32_t bit = 1u << cand_slot(c[r], M);
-                ok &= (used & bit) == 0;
-                used |= bit;
+                const uint32_t sl = cand_slot<B>(c[r], M), bit = 1u << (sl & 31);
+                uint32_t u = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) u |= (sl >> 5) == (uint32_t)w ? used[w] : 0u;
+                ok &= (u & bit) == 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) used[w] |= (sl >> 5) == (uint32_t)w ? bit : 0u;
             }
         }
         if (ok) { mult[i] = M; return; }
@@ -223,14 +233,14 @@ __global__ void k_cand_hash(const uint32_t* __restrict__ knn32, uint32_t n, int 
 // Classic mode reads tau from the candidate-edge pheromone table T instead.
 // Output: packed {c_r, w} rows, the only table the construction kernel reads.
 template <int KMAX, bool LIVE, bool HASH>
-__global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__ knn32, const float* __restrict__ eta,
+__global__ void __launch_bounds__(256, KMAX > 16 ? 1 : 2) k_weights(const uint32_t* __restrict__ knn32, const float* __restrict__ eta,
                                                  const uint2* __restrict__ nbr, const int64_t* __restrict__ lb_len,
                                                  const uint8_t* __restrict__ has_lb, const int64_t* __restrict__ g_len,
                                                  const unsigned long long* __restrict__ gkey,
                                                  const double* __restrict__ T, const uint32_t* __restrict__ mult,
                                                  uint32_t n, uint32_t m, int k,
                                                  int kp, double alpha, double tau0, uint2* __restrict__ cand) {
-    extern __shared__ double ratio[];  // m ratios | HASH: slot table [32][blockDim] u32, acc [KMAX][blockDim] f64
+    extern __shared__ double ratio[];  // m ratios | HASH: slot table [2^B][blockDim] u32, acc [KMAX][blockDim] f64
     if (!T) {
         // colony.hpp:159-177 ratios. In async mode (gkey != nullptr) the colony changes under
         // this pass: lengths and g_best are read past L1 (ld.cv), a snapshot at pass start.
@@ -258,15 +268,16 @@ __global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__
         // add can address acc[r] with the r found. Every sum still takes its terms in ant
         // order. The comparison loop below was ALU-bound (91% of the ALU pipe, 32 compares
         // per ant and city; profiles/README.md).
+        constexpr int B = hash_slot_bits(KMAX);
         const uint32_t t = threadIdx.x, bd = blockDim.x;
         uint32_t* tab = reinterpret_cast<uint32_t*>(ratio + m);
-        double* accs = reinterpret_cast<double*>(tab + 32 * bd);
+        double* accs = reinterpret_cast<double*>(tab + (1 << B) * bd);
         const uint32_t M = mult[i];
 #pragma unroll
-        for (int s = 0; s < 32; ++s) tab[s * bd + t] = kNone;
+        for (int s = 0; s < (1 << B); ++s) tab[s * bd + t] = kNone;
 #pragma unroll
         for (int r = 0; r < KMAX; ++r) {
-            if (r < k) tab[cand_slot(c[r], M) * bd + t] = ((uint32_t)r << 27) | c[r];
+            if (r < k) tab[cand_slot<B>(c[r], M) * bd + t] = ((uint32_t)r << 27) | c[r];
             accs[r * bd + t] = 0.0;
         }
         constexpr uint32_t U = 8;
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__
             if (a0 + U < m) fetch(a0 + U, pn, rrn);
 #pragma unroll
             for (uint32_t u = 0; u < U; ++u) {
-                const uint32_t ex = tab[cand_slot(p[u].x, M) * bd + t], ey = tab[cand_slot(p[u].y, M) * bd + t];
+                const uint32_t ex = tab[cand_slot<B>(p[u].x, M) * bd + t], ey = tab[cand_slot<B>(p[u].y, M) * bd + t];
                 if ((ex & 0x07ffffffu) == p[u].x) {
                     double* q = accs + (ex >> 27) * bd + t;
                     *q = __dadd_rn(*q, rr[u]);
@@ -309,8 +320,9 @@ __global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__
         // batch: 1.49 -> see profiles/README.md). The slices are streamed once: evict-first
         // in sync mode, read past L1 in async mode (LIVE), where ants rewrite them meanwhile.
         // prev != next for n >= 3 (a tour of distinct cities), so a candidate matches at
-        // most one of them and one predicated add per candidate does both tests.
-        constexpr uint32_t U = 8;
+        // most one of them and one predicated add per candidate does both tests. Four ants
+        // per batch above 16 candidates keep the sums and pairs in registers (no spills).
+        constexpr uint32_t U = KMAX > 16 ? 4 : 8;
         auto fetch = [&](uint32_t a0, uint2 (&p)[U], double (&rr)[U]) {
 #pragma unroll
             for (uint32_t u = 0; u < U; ++u) {
@@ -340,7 +352,7 @@ __global__ void __launch_bounds__(256, 2) k_weights(const uint32_t* __restrict__
         if (r < k) {
             const double tau = T ? T[(size_t)i * k + r] : __dadd_rn(tau0, acc[r]);
             const float w = __fmul_rn((float)power(alpha, tau), eta[(size_t)i * k + r]);
-            cand[(size_t)i * kp + r] = make_uint2(c[r], __float_as_uint(w));
+            cand[(size_t)i * kp + r] = make_uint2(HASH ? knn32[(size_t)i * kNearRow + r] : c[r], __float_as_uint(w));
         }
     }
 }
@@ -959,7 +971,7 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         }
     }
     n_tie += __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(tie_v, tie_t)) <= tie_tol) ? 1u : 0u;
-    if (n_dec > 0) {  // the single remaining city is appended unscored (construction.hpp:529-535)
+    if (n_dec > 0) {  // the single remaining city is appended unscored (construction.hpp:342-348)
         __syncwarp();
         const uint32_t last = last_unvisited(vis, nw, lane);
         if (lane == 0) out[pos] = last;

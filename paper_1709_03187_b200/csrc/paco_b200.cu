@@ -243,9 +243,11 @@ static size_t construct_smem_need(uint32_t kp, uint32_t nwords, bool async_mode)
     for (int q = 0; q < nk; ++q) st = std::max(st, static_smem(kerns[q]));
     return construct_dyn_smem(nwords) + st;
 }
-// k_weights: ratios (8 B per ant) plus, on the hashed path, 256 threads x (32 slots + km sums)
+// k_weights: ratios (8 B per ant) plus, on the hashed path, per thread 2^B slots and km sums
+static int weights_block(int km, bool hash) { return hash && km > 16 ? 128 : 256; }
 static size_t weights_dyn_smem(uint32_t m, int km, bool hash) {
-    return sizeof(double) * m + (hash ? (sizeof(uint32_t) * 32 + sizeof(double) * km) * 256 : 0);
+    return sizeof(double) * m +
+           (hash ? (sizeof(uint32_t) * (1u << hash_slot_bits(km)) + sizeof(double) * km) * weights_block(km, true) : 0);
 }
 
 static paco_status build_grid(paco_handle* h) {
@@ -425,12 +427,16 @@ static paco_status setup(paco_handle* h) {
     CU(cudaGetLastError());
     int dev_optin = 0;
     CU(cudaDeviceGetAttribute(&dev_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
-    if (h->mode != PACO_MODE_CLASSIC && k <= 16 &&
+    if (h->mode != PACO_MODE_CLASSIC &&
         weights_dyn_smem(h->m, kmax_for(k), true) <= (size_t)dev_optin) {  // candidate perfect hashes for k_weights
         int* dfail = nullptr;
         CU(dalloc(&h->cand_mult, n)); CU(dalloc(&dfail, 1));
         CU(cudaMemsetAsync(dfail, 0, sizeof(int), st));
-        k_cand_hash<<<nb, tb, 0, st>>>(h->knn, n, (int)k, h->cand_mult, dfail);
+        const int km = kmax_for(k);
+        if (km == 8) k_cand_hash<8><<<nb, tb, 0, st>>>(h->knn, n, (int)k, h->cand_mult, dfail);
+        else if (km == 16) k_cand_hash<16><<<nb, tb, 0, st>>>(h->knn, n, (int)k, h->cand_mult, dfail);
+        else if (km == 24) k_cand_hash<24><<<nb, tb, 0, st>>>(h->knn, n, (int)k, h->cand_mult, dfail);
+        else k_cand_hash<32><<<nb, tb, 0, st>>>(h->knn, n, (int)k, h->cand_mult, dfail);
         CU(cudaGetLastError());
         int hf = 0;
         CU(cudaMemcpyAsync(&hf, dfail, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -534,12 +540,13 @@ static cudaEvent_t ev(paco_handle* h, size_t i) {
 }
 
 static paco_status launch_weights(paco_handle* h, cudaStream_t stream = nullptr, const unsigned long long* gkey = nullptr) {
-    const uint32_t n = h->n, tb = 256;
+    const uint32_t n = h->n;
     if (!stream) stream = h->st;
     const double* T = h->mode == PACO_MODE_CLASSIC ? h->T : nullptr;
     const int km = kmax_for(h->k);
-    const bool hash = !T && h->cand_mult != nullptr && km <= 16;  // perfect-hash lookup (k_cand_hash)
-    const size_t smem = T ? 0 : sizeof(double) * h->m + (hash ? (sizeof(uint32_t) * 32 + sizeof(double) * km) * tb : 0);
+    const bool hash = !T && h->cand_mult != nullptr;  // perfect-hash lookup (k_cand_hash)
+    const uint32_t tb = (uint32_t)weights_block(km, hash);
+    const size_t smem = T ? 0 : weights_dyn_smem(h->m, km, hash);
 #define LAUNCH_W3(KM, LIVE, HASH)                                                                          \
     do {                                                                                                   \
         if (smem > 48 * 1024)                                                                              \
@@ -550,9 +557,7 @@ static paco_status launch_weights(paco_handle* h, cudaStream_t stream = nullptr,
     } while (0)
 #define LAUNCH_W2(KM, LIVE) do { if (hash) LAUNCH_W3(KM, LIVE, true); else LAUNCH_W3(KM, LIVE, false); } while (0)
 #define LAUNCH_W(KM) do { if (gkey) LAUNCH_W2(KM, true); else LAUNCH_W2(KM, false); } while (0)
-    if (km == 8) LAUNCH_W(8); else if (km == 16) LAUNCH_W(16);
-    else if (km == 24) { if (gkey) LAUNCH_W3(24, true, false); else LAUNCH_W3(24, false, false); }
-    else { if (gkey) LAUNCH_W3(32, true, false); else LAUNCH_W3(32, false, false); }
+    if (km == 8) LAUNCH_W(8); else if (km == 16) LAUNCH_W(16); else if (km == 24) LAUNCH_W(24); else LAUNCH_W(32);
 #undef LAUNCH_W
 #undef LAUNCH_W2
 #undef LAUNCH_W3

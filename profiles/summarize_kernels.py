@@ -23,8 +23,11 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns
 
 
 def main() -> None:
-    raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True,
-                         check=True).stdout
+    if sys.argv[1].endswith(".csv"):  # a `--page raw --csv` export saved on the GPU box
+        raw = open(sys.argv[1]).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units, data = rows[0], rows[1], rows[2:]
     ik = hdr.index("Kernel Name")
