@@ -143,6 +143,15 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def instance_sha256(inst) -> str:
+    """sha256 of the instance as TSPLIB text (emit_tsplib, instance.hpp:251-261)."""
+    import hashlib
+
+    from paper_1709_03187_b200.instances import emit_tsplib
+
+    return hashlib.sha256(emit_tsplib(inst).encode()).hexdigest()
+
+
 def load_json(path):
     try:
         with open(path) as f:
@@ -299,7 +308,8 @@ def run_ours(args, rank, world, local):
                    "step": "one synchronous ACO iteration (weights, construction, completion step)",
                    "l2": "flushed (512 MiB write) before every timed step; per-step working set "
                          "(neighbour slices + tours) exceeds L2",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": f"replicas x{world}",
+                   "instance_sha256": instance_sha256(inst)},
         "tours_per_s": tours_sum / (tmax / 1e3),
         "fallback_frac": fallbacks / max(1, decisions),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
