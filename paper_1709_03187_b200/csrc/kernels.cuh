@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(256, KMAX > 16 ? 1 : 2) k_weights(const uint32
 // ============================================================ K2: construction
 struct ConstructArgs {
     const uint2* cand;        // n*k {city, f32 weight}
+    const uint32_t* order;    // CTA -> ant (k_ant_order), nullptr = identity
     const uint32_t* knn32;    // n*kNearRow nearest cities by (d^2, orig), kNone padded
     const double2* xy;        // internal coordinates
     const uint32_t* orig_of;  // internal -> original (fallback tie-break)
@@ -1064,7 +1065,7 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];  // fallback list | visited bitmap | warm scratch
     __shared__ FallbackCtx fctx;
     init_fallback_ctx(a, fctx);
-    const uint32_t ant = a.force ? a.force_ant : blockIdx.x;
+    const uint32_t ant = a.force ? a.force_ant : (a.order ? a.order[blockIdx.x] : blockIdx.x);
     bool partial;
     uint32_t cnt[5];
 #ifdef PACO_ANTPROF
@@ -1341,6 +1342,56 @@ __global__ void __launch_bounds__(512, 1) k_two_opt(uint32_t* __restrict__ tours
         if (threadIdx.x == 0) { new_len[a] += d; flag[a] = 0; atomicAdd(moves, (unsigned long long)mv); }
         __syncthreads();
     }
+}
+
+// Launch order of the synchronous construction (K2): every ant's decision count this
+// iteration follows from its draws alone (coin, start_pos, m_mod: slots 0-2), so the ants
+// are sorted by it, longest first. CTAs are handed out in index order, so the longest
+// ants land on distinct SMs and share them with ever shorter ones, which finish early:
+// the critical ant runs most of its construction with fewer co-resident warps. Results do
+// not depend on the order. One CTA of 1024 threads, bitonic sort of (decisions, ant)
+// keys over the next power of two >= m (m <= 4096; larger colonies keep the identity).
+__global__ void __launch_bounds__(1024) k_ant_order(const uint32_t* __restrict__ words, uint64_t stride,
+                                                    uint64_t seed, uint64_t iter, uint32_t n, uint32_t m,
+                                                    double eff_pp, double mmf, int seeding, uint32_t* __restrict__ order) {
+    __shared__ unsigned long long key[4096];
+    uint32_t P = 1;
+    while (P < m) P <<= 1;
+    const uint2 k2 = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    for (uint32_t a = threadIdx.x; a < P; a += blockDim.x) {
+        unsigned long long kk = 0ull;  // padding sorts last
+        if (a < m) {
+            uint32_t w0, w2;
+            if (words) { w0 = words[(size_t)a * stride]; w2 = words[(size_t)a * stride + 2]; }
+            else {
+                const uint4 v = philox10(make_uint4(0u, a, (uint32_t)iter, (uint32_t)(iter >> 32)), k2);
+                w0 = v.x; w2 = v.z;
+            }
+            uint32_t dec = n - 1;
+            if (!seeding && u01_f64(w0) < eff_pp) {  // partial: m_mod decisions (construction.hpp:354-362)
+                double capd = floor(mmf * (double)n);
+                if (capd < 2.0) capd = 2.0;
+                dec = 2 + below(w2, (uint32_t)capd - 1);
+            }
+            kk = ((unsigned long long)dec << 32) | (0xffffffffu - a);  // longest first, then lower ant
+        }
+        key[a] = kk;
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const bool desc = (i & k) == 0;
+                    const unsigned long long x = key[i], y = key[l];
+                    if (desc ? x < y : x > y) { key[i] = y; key[l] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) order[i] = 0xffffffffu - (uint32_t)key[i];
 }
 
 // reference-order tour -> internal ids (host offers), and internal -> original on readback

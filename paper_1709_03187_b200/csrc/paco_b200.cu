@@ -112,6 +112,7 @@ struct paco_handle {
     uint32_t two_opt_ctas = 0;
     float* eta = nullptr;
     uint2* cand = nullptr;
+    uint32_t* order = nullptr;  // CTA -> ant launch order of K2 (k_ant_order), m <= 4096
     uint32_t* tours = nullptr;
     uint8_t *lb_sel = nullptr, *has_lb = nullptr, *improved = nullptr, *partial = nullptr;
     int64_t *new_len = nullptr, *lb_len = nullptr, *g_len = nullptr;
@@ -145,7 +146,7 @@ struct paco_handle {
         if (st) cudaStreamSynchronize(st);  // nothing may still use the buffers returned below
         if (st2) cudaStreamSynchronize(st2);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
-                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words, two_opt_flag, two_opt_edges, two_opt_txy,
+                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words, order, two_opt_flag, two_opt_edges, two_opt_txy,
                         scratch_u32, scratch_u64, rng, ratio, Tfull, eta_tab, cand_mult};
         for (void* p : ptrs) dfree(p);
         for (auto e : evpool) cudaEventDestroy(e);
@@ -306,6 +307,9 @@ static paco_status alloc_colony(paco_handle* h) {
     CU(cudaMemsetAsync(h->counters, 0, 16 * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(h->err, 0, sizeof(int), st));
     if (h->mode == PACO_MODE_CLASSIC) CU(dalloc(&h->cur_nbr, (size_t)m * n));
+#ifndef PACO_NO_ORDER
+    if (!h->ir && !h->async_mode && m <= 4096) CU(dalloc(&h->order, m));
+#endif
     if (!h->ir && !h->async_mode && h->cfg.two_opt_prob > 0.0) {
         h->two_opt_ctas = std::min<uint32_t>(m, 64);
         CU(dalloc(&h->two_opt_flag, m));
@@ -755,7 +759,18 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
         paco_status s = h->ir ? launch_ratios(h) : launch_weights(h);
         if (s != PACO_OK) return s;
         CU(cudaEventRecord(ev(h, e1), h->st));
-        s = h->ir ? launch_construct_ir(h, seeding) : launch_construct(h, construct_args(h, seeding), m);
+        if (h->ir) {
+            s = launch_construct_ir(h, seeding);
+        } else {
+            ConstructArgs ca = construct_args(h, seeding);
+            if (h->order && !seeding && h->mode == PACO_MODE_PARTIAL) {  // longest ants first (k_ant_order)
+                k_ant_order<<<1, 1024, 0, h->st>>>(ca.words, ca.stride, h->cfg.seed, h->iter, n, m, ca.eff_pp, ca.mmf,
+                                                   0, h->order);
+                CU(cudaGetLastError());
+                ca.order = h->order;
+            }
+            s = launch_construct(h, ca, m);
+        }
         if (s != PACO_OK) return s;
         if (h->two_opt_flag) {  // maybe_two_opt's searches, one CTA per flagged tour (k_two_opt)
             k_two_opt<<<h->two_opt_ctas, 512, 0, h->st>>>(h->tours, h->lb_sel, h->two_opt_flag, h->new_len, n, m,
