@@ -62,7 +62,8 @@ def main() -> None:
         if os.path.exists(OUT):
             with open(OUT) as f:
                 db = json.load(f)
-        db.setdefault(a.config, {})[str(seed)] = rec
+        key = a.config if iters == spec["iterations"] else f"{a.config}@{iters}"  # shortened budgets apart
+        db.setdefault(key, {})[str(seed)] = rec
         with open(OUT, "w") as f:
             json.dump(db, f, indent=1, sort_keys=True)
         print(json.dumps(rec), flush=True)
