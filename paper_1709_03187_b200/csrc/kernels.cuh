@@ -1344,6 +1344,40 @@ __global__ void __launch_bounds__(512, 1) k_two_opt(uint32_t* __restrict__ tours
     }
 }
 
+// maybe_two_opt's searches when few tours are flagged (the paper's p = 0.001: about one
+// search per iteration): one thread-block cluster of CS CTAs per flagged tour
+// (two_opt_cluster), clusters striding over the ants. Same moves as k_two_opt.
+__global__ void __launch_bounds__(512, 1) k_two_opt_cluster(uint32_t* __restrict__ tours, const uint8_t* __restrict__ lb_sel,
+                                                          uint8_t* __restrict__ flag, int64_t* __restrict__ new_len,
+                                                          uint32_t n, uint32_t m, uint32_t window,
+                                                          const double2* __restrict__ xy, int32_t* __restrict__ edges,
+                                                          double2* __restrict__ txy, unsigned long long* __restrict__ moves,
+                                                          uint32_t stage_cap) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ TwoOptShared sh;
+    extern __shared__ __align__(16) unsigned char stage_raw[];  // stage_cap double2 | int32 | u32
+    double2* s_txy = reinterpret_cast<double2*>(stage_raw);
+    int32_t* s_edge = reinterpret_cast<int32_t*>(stage_raw + (size_t)stage_cap * sizeof(double2));
+    uint32_t* s_o = reinterpret_cast<uint32_t*>(s_edge + stage_cap);
+    const uint32_t CS = cl.num_blocks();
+    const uint32_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+    int32_t* e = edges + (size_t)cid * n;
+    double2* tx = txy + (size_t)cid * n;
+    for (uint32_t a = cid; a < m; a += ncl) {
+        if (!flag[a]) continue;  // cluster-uniform
+        uint32_t* o = tours + ((size_t)a * 2 + (1 - lb_sel[a])) * n;
+        uint32_t mv = 0;
+        const long long d = two_opt_cluster(cl, o, n, window, xy, e, tx, sh, s_txy, s_edge, s_o, stage_cap, &mv);
+        if (cl.block_rank() == 0 && threadIdx.x == 0) {  // every CTA read flag[a] before the search
+            new_len[a] += d;
+            flag[a] = 0;
+            atomicAdd(moves, (unsigned long long)mv);
+        }
+        cl.sync();  // the caches are reused for the cluster's next tour
+    }
+}
+
 // Launch order of the synchronous construction (K2): every ant's decision count this
 // iteration follows from its draws alone (coin, start_pos, m_mod: slots 0-2), so the ants
 // are sorted by it, longest first. CTAs are handed out in index order, so the longest

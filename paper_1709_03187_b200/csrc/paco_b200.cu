@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -110,6 +111,9 @@ struct paco_handle {
     int32_t* two_opt_edges = nullptr;
     double2* two_opt_txy = nullptr;
     uint32_t two_opt_ctas = 0;
+    uint32_t two_opt_cs = 0, two_opt_clusters = 0;  // k_two_opt_cluster: cluster size, clusters (0 = unavailable)
+    uint32_t two_opt_stage = 0;                      // positions staged in shared memory per round (0 = none)
+    bool two_opt_use_cluster = false;
     float* eta = nullptr;
     uint2* cand = nullptr;
     uint32_t* order = nullptr;  // CTA -> ant launch order of K2 (k_ant_order), m <= 4096
@@ -285,6 +289,56 @@ static size_t ir_smem_bytes(uint32_t n, uint32_t m, uint32_t nwords, int mode) {
 }
 
 // colony state shared by both selection rules
+// k_two_opt_cluster's shape: the largest cluster (16 CTAs of 512 threads, non-portable,
+// else 8) the device can co-schedule, as many clusters as fit at once (at most the cache
+// slots). The searches go to clusters when the expected number of flagged tours per
+// iteration (m * two_opt_prob) is at most the number of clusters - the paper's setting,
+// p = 0.001 - and to one CTA per tour (k_two_opt) otherwise. PACO_TWO_OPT_PATH=cta|cluster
+// overrides the choice (tests).
+constexpr uint32_t kTwoOptStageMax = 2048;  // 48 KB of shared memory per CTA
+static void pick_two_opt_cluster(paco_handle* h) {
+    h->two_opt_cs = 0; h->two_opt_clusters = 0; h->two_opt_use_cluster = false;
+    if (cudaFuncSetAttribute(k_two_opt_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(k_two_opt_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kTwoOptStageMax * (sizeof(double2) + sizeof(int32_t) + sizeof(uint32_t)))) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    uint32_t sizes[2] = {16u, 8u};
+    if (const char* e = std::getenv("PACO_TWO_OPT_CS")) sizes[0] = sizes[1] = (uint32_t)std::atoi(e);
+    for (uint32_t cs : sizes) {
+        cudaLaunchConfig_t lc = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        lc.gridDim = dim3(cs); lc.blockDim = dim3(512); lc.attrs = at; lc.numAttrs = 1;
+        lc.dynamicSmemBytes = (size_t)kTwoOptStageMax * (sizeof(double2) + sizeof(int32_t) + sizeof(uint32_t));
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, k_two_opt_cluster, &lc) == cudaSuccess && nc >= 1) {
+            h->two_opt_cs = cs;
+            h->two_opt_clusters = std::min<uint32_t>((uint32_t)nc, h->two_opt_ctas);
+            break;
+        }
+        cudaGetLastError();
+    }
+    if (!h->two_opt_clusters) return;
+    // a round reads at most 2W + R + 2 positions (R forward rows, about two cells per thread)
+    const uint64_t weff = h->cfg.two_opt_window == 0 ? h->n - 1 : h->cfg.two_opt_window;
+    const uint64_t G = (uint64_t)h->two_opt_cs * 512, R = weff >= 2 * G ? 1 : 2 * G / weff;
+    const uint64_t span = 2 * weff + R + 2;
+    uint32_t cap = 256;
+    while (cap < span) cap *= 2;
+    h->two_opt_stage = cap <= kTwoOptStageMax ? cap : 0u;  // a power of two (ring slots)
+    h->two_opt_use_cluster = (double)h->m * h->cfg.two_opt_prob <= (double)h->two_opt_clusters;
+    if (const char* e = std::getenv("PACO_TWO_OPT_PATH")) {
+        if (!std::strcmp(e, "cta")) h->two_opt_use_cluster = false;
+        if (!std::strcmp(e, "cluster")) h->two_opt_use_cluster = true;
+        if (!std::strcmp(e, "verbose") || std::getenv("PACO_TWO_OPT_VERBOSE"))
+            std::fprintf(stderr, "k_two_opt_cluster: %u CTAs per cluster, %u clusters, stage %u, in use: %d\n",
+                         h->two_opt_cs, h->two_opt_clusters, h->two_opt_stage, (int)h->two_opt_use_cluster);
+    }
+}
+
 static paco_status alloc_colony(paco_handle* h) {
     const uint32_t n = h->n, m = h->m;
     cudaStream_t st = h->st;
@@ -312,6 +366,7 @@ static paco_status alloc_colony(paco_handle* h) {
 #endif
     if (!h->ir && !h->async_mode && h->cfg.two_opt_prob > 0.0) {
         h->two_opt_ctas = std::min<uint32_t>(m, 64);
+        pick_two_opt_cluster(h);
         CU(dalloc(&h->two_opt_flag, m));
         CU(dalloc(&h->two_opt_edges, (size_t)h->two_opt_ctas * n));
         CU(dalloc(&h->two_opt_txy, (size_t)h->two_opt_ctas * n));
@@ -772,7 +827,18 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
             s = launch_construct(h, ca, m);
         }
         if (s != PACO_OK) return s;
-        if (h->two_opt_flag) {  // maybe_two_opt's searches, one CTA per flagged tour (k_two_opt)
+        if (h->two_opt_flag && h->two_opt_use_cluster) {  // maybe_two_opt's searches, a cluster per tour
+            cudaLaunchConfig_t lc = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = h->two_opt_cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            lc.gridDim = dim3(h->two_opt_cs * h->two_opt_clusters); lc.blockDim = dim3(512);
+            lc.dynamicSmemBytes = (size_t)h->two_opt_stage * (sizeof(double2) + sizeof(int32_t) + sizeof(uint32_t));
+            lc.stream = h->st; lc.attrs = at; lc.numAttrs = 1;
+            CU(cudaLaunchKernelEx(&lc, k_two_opt_cluster, h->tours, (const uint8_t*)h->lb_sel, h->two_opt_flag,
+                                  h->new_len, n, m, h->cfg.two_opt_window, (const double2*)h->xy, h->two_opt_edges,
+                                  h->two_opt_txy, h->counters + 10, h->two_opt_stage));
+        } else if (h->two_opt_flag) {  // maybe_two_opt's searches, one CTA per flagged tour (k_two_opt)
             k_two_opt<<<h->two_opt_ctas, 512, 0, h->st>>>(h->tours, h->lb_sel, h->two_opt_flag, h->new_len, n, m,
                                                           h->cfg.two_opt_window, h->xy, h->two_opt_edges,
                                                           h->two_opt_txy, h->counters + 10);
@@ -947,6 +1013,9 @@ paco_status paco_get_candidates(paco_handle* h, uint32_t* knn, float* weights, u
     return PACO_OK;
 }
 
+#ifdef PACO_2OPT_PROF
+extern "C" void paco_debug_2opt(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_2opt_prof, sizeof(unsigned long long) * 8); }
+#endif
 #ifdef PACO_DEBUG_SYMS
 #ifdef PACO_ANTPROF
 extern "C" void paco_debug_ant(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ant, sizeof(unsigned long long) * 4096 * 6); }

@@ -242,6 +242,147 @@ __global__ void __launch_bounds__(32, 1) dec(const uint2* __restrict__ cand, con
 
 std::vector<uint32_t> g_ref;
 
+// HELPER: warp 0 builds the tour with no L1-warming copies of its own; warp 1 of the same
+// CTA watches the city warp 0 has just moved to (a shared-memory sequence number) and pulls
+// the rows of all of that city's candidates into L1 with cp.async.ca. GVIS: the visited
+// bitmap in global memory (L1-cached byte loads / stores) instead of shared memory, with
+// warp 0's own cp.async warming. Both test whether the bitmap probe (LDS) waits behind the
+// same warp's LDGSTS.
+template <int V>
+__global__ void __launch_bounds__(64, 1) dec_helper(const uint2* __restrict__ cand, uint32_t n, uint32_t D,
+                                                    uint32_t* tours, long long* cyc, unsigned char* gvis_all) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, ant = blockIdx.x, nw = (n + 31) / 32;
+    constexpr bool GV = (V & 1) != 0;   // global bitmap
+    constexpr bool HLP = (V & 2) != 0;  // helper warp warms
+    volatile uint32_t* seq = reinterpret_cast<volatile uint32_t*>(smem);  // [0] seq, [1] city, [2] done
+    uint32_t* vis = reinterpret_cast<uint32_t*>(smem + 64);
+    unsigned char* gvis = gvis_all + (size_t)ant * nw * 4;
+    if (warp == 0) {
+        for (uint32_t w = lane; w < nw; w += 32) { vis[w] = 0u; if (GV) reinterpret_cast<uint32_t*>(gvis)[w] = 0u; }
+    }
+    if (threadIdx.x == 0) { seq[0] = 0; seq[1] = 0; seq[2] = 0; }
+    __syncthreads();
+    const uint32_t vis_s = (uint32_t)__cvta_generic_to_shared(vis);
+    const uint32_t warm_s = ((vis_s + nw * 4 + 15) & ~15u) + (threadIdx.x & 63) * 16;
+    uint32_t cur = (ant * 977u) % n;
+    if (warp == 1) {
+        if (!HLP) return;
+        uint32_t last = 0;
+        for (;;) {
+            uint32_t s0;
+            do { s0 = seq[0]; } while (s0 == last && !seq[2]);
+            if (seq[2]) break;
+            last = s0;
+            const uint32_t c = seq[1];
+            const uint2 e = ldg_u64_if(cand + (size_t)c * 16 + lane, lane < 16, make_uint2(c, 0u));
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(cand + (size_t)e.x * 16);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cp_async16_if(warm_s, src + 32 * q, lane < 16);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        return;
+    }
+    if (lane == 0) { vis[cur >> 5] |= 1u << (cur & 31); if (GV) gvis[cur >> 3] |= 1u << (cur & 7); }
+    __syncwarp();
+    uint32_t* out = tours + (size_t)ant * D;
+    const uint2 key = make_uint2(7u, 0u);
+    const bool lane_in = lane < 16;
+    const uint2* row_base = cand + lane;
+    uint2 e_pre = ldg_u64_if(row_base + (size_t)cur * 16, lane_in, make_uint2(cur, 0u));
+    uint32_t n_tie = 0;
+    float tie_v = 0.0f, tie_t = 0.0f, tie_tol = -1.0f;
+    const long long t0 = clock64();
+    for (uint32_t b0 = 0; b0 < D; b0 += 128) {
+        const uint4 pb = philox10(make_uint4(1 + (b0 >> 2) + lane, ant, 0, 0), key);
+        const uint32_t b1 = b0 + 128 < D ? b0 + 128 : D;
+#pragma unroll 2
+        for (uint32_t t = b0; t < b1; ++t) {
+            __syncwarp();
+            const uint2 e = e_pre;
+            n_tie += __ballot_sync(kFull, lane_in && fabsf(__fsub_rn(tie_v, tie_t)) <= tie_tol) ? 1u : 0u;
+            const uint32_t vw_addr = vis_s + (e.x >> 3);
+            uint32_t vw;
+            if (GV) {
+                asm volatile("ld.global.u8 %0, [%1];" : "=r"(vw) : "l"(gvis + (e.x >> 3)));
+            } else {
+                vw = lds_u8(vw_addr);
+            }
+            const uint32_t uw = __shfl_sync(kFull, pick_word(pb, t & 3), (t & 127) >> 2);
+            const uint32_t bit = 1u << (e.x & 7);
+            const bool fe = lane_in && !(vw & bit);
+            if (!HLP) {
+                const unsigned char* src = reinterpret_cast<const unsigned char*>(cand + (size_t)e.x * 16);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) cp_async16_if(warm_s, src + 32 * c, fe);
+            }
+            const unsigned feas = __ballot_sync(kFull, fe);
+            const bool is_last = lane == 31u - __clz(feas);
+            const uint32_t pick_key = (lane << 27) | e.x;
+            float v = fe ? __uint_as_float(e.y) : 0.0f;
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+                const float y = __shfl_up_sync(kFull, v, 1u << st);
+                if (lane >= (1u << st)) v = __fadd_rn(v, y);
+            }
+            const float S = __shfl_sync(kFull, v, 15);
+            uint32_t next;
+            if (feas) {
+                const float u = u01_f32(uw);
+                const float target = __fmul_rn(u, S);
+                const float tol = __fmul_rn(1e-6f, S);
+                const bool win = (fe & (v > target)) | is_last;
+                const uint32_t kw = __reduce_min_sync(kFull, win ? pick_key : kNone);
+                tie_v = v; tie_t = target; tie_tol = tol;
+                const uint32_t r = kw >> 27;
+                next = kw & 0x07ffffffu;
+                if (GV) {
+                    if (lane == r) asm volatile("st.global.u8 [%0], %1;" :: "l"(gvis + (e.x >> 3)), "r"(vw | bit) : "memory");
+                } else {
+                    sts_u8_if(vw_addr, vw | bit, lane == r);
+                }
+            } else {
+                next = (uint32_t)(((uint64_t)(cur + 1) * 2654435761ull) % n);
+                tie_tol = -1.0f;
+                if (lane == 0) {
+                    vis[next >> 5] |= 1u << (next & 31);
+                    if (GV) gvis[next >> 3] |= 1u << (next & 7);
+                }
+            }
+            if (HLP && lane == 0) { seq[1] = next; __threadfence_block(); seq[0] = t + 1; }
+            e_pre = ldg_u64_if(row_base + (size_t)next * 16, lane_in, make_uint2(next, 0u));
+            stg_u32_if(out + t, next, lane == 0);
+            cur = next;
+        }
+    }
+    const long long t1 = clock64();
+    if (lane == 0) { seq[2] = 1; cyc[ant] = t1 - t0 + (n_tie == 0xffffffffu); }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <int V>
+void run_helper(const char* name, const uint2* cand, uint32_t n, uint32_t D, uint32_t m, uint32_t* tours, long long* cyc,
+                unsigned char* gvis) {
+    const size_t smem = 64 + ((n + 31) / 32) * 4 + 16 + 1024;
+    cudaFuncSetAttribute(dec_helper<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(dec_helper<V>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    dec_helper<V><<<m, 64, smem>>>(cand, n, D, tours, cyc, gvis);
+    cudaEventRecord(a);
+    dec_helper<V><<<m, 64, smem>>>(cand, n, D, tours, cyc, gvis);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    std::vector<long long> h(m); cudaMemcpy(h.data(), cyc, m * 8, cudaMemcpyDeviceToHost);
+    double mean = 0, mx = 0; for (auto v : h) { mean += v; mx = v > mx ? v : mx; }
+    mean /= m;
+    std::vector<uint32_t> got((size_t)m * D);
+    cudaMemcpy(got.data(), tours, got.size() * 4, cudaMemcpyDeviceToHost);
+    const char* same = "";
+    if (m == 1024) same = (g_ref == got) ? "same tours" : "TOURS DIFFER";
+    printf("%-22s m=%-4u %6.1f cyc/dec (max ant %6.1f) %8.3f ms %s %s\n", name, m, mean / D, mx / D, ms, same,
+           cudaGetErrorString(cudaGetLastError()));
+}
+
 template <int V>
 void run(const char* name, const uint2* cand, const uint32_t* split, uint32_t n, uint32_t D, uint32_t m, uint32_t* tours,
          long long* cyc, unsigned long long* seg, bool reset_ref) {
@@ -297,6 +438,14 @@ int main() {
     printf("n=%u m=%u D=%u\n", n, m, D);
     run<BASE | TM>("base timed", cand, split, n, D, 1, tours, cyc, seg, true);
     run<ROW1 | TM>("row f32 timed", cand, split, n, D, 1, tours, cyc, seg, true);
+    unsigned char* gvis; cudaMalloc(&gvis, (size_t)2048 * ((n + 31) / 32) * 4);
+    for (uint32_t mm : {1u, 148u, 1024u}) {
+        run<BASE>("base (engine loop)", cand, split, n, D, mm, tours, cyc, seg, true);
+        run_helper<0>("2-warp CTA, own warm", cand, n, D, mm, tours, cyc, gvis);
+        run_helper<2>("helper-warp warming", cand, n, D, mm, tours, cyc, gvis);
+        run_helper<1>("global bitmap", cand, n, D, mm, tours, cyc, gvis);
+        run_helper<3>("global bitmap + helper", cand, n, D, mm, tours, cyc, gvis);
+    }
     run<BASE | TM | NOWARM>("base nowarm timed", cand, split, n, D, 1, tours, cyc, seg, true);
     run<BASE | TM | WLDG>("base ldg-warm timed", cand, split, n, D, 1, tours, cyc, seg, true);
     run<BASE | TM>("base timed", cand, split, n, D, 1024, tours, cyc, seg, true);

@@ -133,20 +133,26 @@ def test_classic_mode():
     col, ref = lockstep(inst, 12, mode=Mode.classic_aco, ants=20, candidates=20, rho=0.5)
 
 
+@pytest.mark.parametrize("path", ["cta", "cluster"])
 @pytest.mark.parametrize("p2,w2", [(0.25, 0), (0.5, 12)])
-def test_two_opt_after_construction(p2, w2):
+def test_two_opt_after_construction(p2, w2, path, monkeypatch):
     """maybe_two_opt (two_opt.hpp:71-76) on the north-star rule: draw slot 3, first-improvement
-    2-opt (windowed or not) on the built tour, identical to O2."""
+    2-opt (windowed or not) on the built tour, identical to O2 - through k_two_opt (a CTA per
+    searched tour) and k_two_opt_cluster (a thread-block cluster per searched tour)."""
+    monkeypatch.setenv("PACO_TWO_OPT_PATH", path)
     inst = make_config_instance("C1", n=250)
     col, ref = lockstep(inst, 8, ants=12, candidates=10, two_opt_prob=p2, two_opt_window=w2, seed=6)
     assert col.counters()["two_opts"] == ref.counters()["two_opts"] > 0
 
 
+@pytest.mark.parametrize("path", ["cta", "cluster"])
 @pytest.mark.parametrize("n,w2", [(3000, 100), (1500, 0)])
-def test_two_opt_exact_sequence_on_longer_tours(n, w2):
-    """The synchronous engine's k_two_opt (CTA-wide scan, restart at i - W after a move, squared-
-    distance filter) ends every search on O2's tour, and O2 restates two_opt.hpp:28-67 literally
+def test_two_opt_exact_sequence_on_longer_tours(n, w2, path, monkeypatch):
+    """The synchronous engine's searches (k_two_opt: CTA-wide scan; k_two_opt_cluster: the scan
+    spread over a thread-block cluster; both restart at i - W after a move and use the squared-
+    distance filter) end every search on O2's tour, and O2 restates two_opt.hpp:28-67 literally
     (restart from i = 0 after every move): the same move sequence, hence the same local optimum."""
+    monkeypatch.setenv("PACO_TWO_OPT_PATH", path)
     inst = make_config_instance("C2", n=n)
     col, ref = lockstep(inst, 4, ants=16, candidates=16, two_opt_prob=0.3, two_opt_window=w2, seed=9)
     assert col.counters()["two_opts"] == ref.counters()["two_opts"] > 0
