@@ -152,6 +152,30 @@ def instance_sha256(inst) -> str:
     return hashlib.sha256(emit_tsplib(inst).encode()).hexdigest()
 
 
+# Dependent latencies of the operations on one decision's chain, measured on a B200
+# (profiles/r01_ubench_latencies.txt: ub_latencies.cu; redux: ub_redux.cu), in SM cycles.
+CHAIN_LATENCY = {"ldg_l1_hit": 66, "lds": 33, "shfl_up_fadd": 33, "shfl_idx": 36, "redux_min": 22}
+
+
+def latency_roofline(spec, k, construct_ms, sm_mhz):
+    """The synchronous iteration is one full construction long (n - 1 dependent decisions of
+    one ant): the construction kernel's time per critical-chain
+    decision against the sum of the measured latencies on that chain (row load from L1,
+    bitmap probe, ceil(log2 k) shuffle-scan levels, the total's shuffle, the pick's
+    reduction) - a floor of this design with zero issue overhead and no fallbacks."""
+    if not sm_mhz:
+        return None
+    levels = max(1, (k - 1).bit_length())
+    c = CHAIN_LATENCY
+    floor = c["ldg_l1_hit"] + c["lds"] + levels * c["shfl_up_fadd"] + c["shfl_idx"] + c["redux_min"]
+    achieved = construct_ms * 1e-3 * sm_mhz * 1e6 / (spec["n"] - 1)
+    return {"bound": "latency", "unit": "cycles per decision of the critical (full-construction) ant",
+            "achieved": achieved, "floor": floor, "frac": floor / achieved,
+            "floor_terms": {**c, "scan_levels": levels},
+            "note": "construction-kernel time x SM clock / (n - 1); floor = sum of the chain's measured "
+                    "dependent latencies (profiles/r01_ubench_latencies.txt, ub_redux.cu)"}
+
+
 def load_json(path):
     try:
         with open(path) as f:
@@ -276,6 +300,8 @@ def run_ours(args, rank, world, local):
     l2peak = load_json(os.path.join(ROOT, "profiles", "l2_peak.json"))
     l2_gbs = l2peak.get("l2_read_gbs")
     dec_per_iter = decisions / args.steps
+    clk = clocks.summary()
+    latency = latency_roofline(spec, k, c_ms_avg, clk.get("sm_mhz"))
     cpu = port = None
     host = {"cpu_model": cpu_model(), "threads": os.cpu_count() or 1}
     if world == 1 and not args.no_cpu:
@@ -325,7 +351,8 @@ def run_ours(args, rank, world, local):
                             "peak_source": "profiles/l2_peak.json (ub_l2_bw.cu, L2-resident read bandwidth "
                                            "measured on a B200)" if l2_gbs else None,
                             "note": "the per-decision tables (candidate rows, 25.6 MB at C5) are L1/L2-resident: "
-                                    "same algorithmic bytes against the L2 bandwidth"}},
+                                    "same algorithmic bytes against the L2 bandwidth"},
+                     "latency": latency},
         "cpu_baseline": cpu,
         "cpu_baseline_port": port,
         "host": {**host, "gpu_iteration_ms": tmax / args.steps,
@@ -343,7 +370,7 @@ def run_ours(args, rank, world, local):
                   "ms": a_ms, "note": "synchronous=False (engine.hpp:213-244): one barrier-free launch for the "
                                       "config's iteration budget after seeding; weights rebuilt concurrently"},
         "gpu_launches": 4 * args.steps,
-        "clocks": clocks.summary(),
+        "clocks": clk,
     }
     print(json.dumps(line), flush=True)
     return 0

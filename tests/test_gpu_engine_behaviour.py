@@ -287,6 +287,8 @@ def test_bench_line_contract():
     assert d["value"] > 0 and d["steps"] == 2 and d["warmup"] == 3 and d["n_gpus"] == 1
     assert d["gpu_launches"] == 4 * 2
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1
+    lat = d["roofline"]["latency"]  # null only when no SM clock was sampled
+    assert lat is None or (lat["bound"] == "latency" and 0 < lat["frac"] <= 1.5 and lat["floor_terms"]["scan_levels"] == 5)
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert "workload" in d["config"] and "model" not in d["config"]
     # traffic is the committed ncu capture of THIS config, or null (never another config's)
