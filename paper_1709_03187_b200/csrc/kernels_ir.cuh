@@ -39,10 +39,20 @@ __device__ __forceinline__ uint32_t xo_below(uint64_t s[4], uint32_t bound) {
     }
 }
 
+// the construction kernel's per-city tau^alpha array in shared memory is padded by one
+// slot per 32 cities, so that lanes reading the 32 cities of their own word (stride 32)
+// hit different banks
+__host__ __device__ inline uint32_t accx(uint32_t j) { return j + (j >> 5); }
+__host__ __device__ inline uint32_t ir_acc_slots(uint32_t n) { return n + (n >> 5) + 1; }
+
+struct IrJump;
 struct IrArgs {
     const double2* xy;        // original order
     const uint2* nbr;         // m*n (prev, next) of each ant's l_best (P-ACO)
     const double* ratio;      // m g/l ratios snapshotted for this iteration (0 = no tour)
+    const uint32_t* tl_city;  // P-ACO: n*2m touched cities of each city's begin_step (k_ir_touched)
+    const double* tl_tau;     // n*2m their tau^alpha
+    const uint32_t* tl_count; // n
     const double* T;          // classic: n*n pheromone matrix, else nullptr
     const float* eta_tab;     // n*n eta^beta as f32 (the reference's table path, n <= 5000), else nullptr
     uint64_t* rng;            // m*4 xoshiro256++ states, carried across iterations
@@ -52,6 +62,7 @@ struct IrArgs {
     uint8_t* partial_flag;
     unsigned long long* counters;  // decisions, fallbacks, ties, forced, full, partial, iter, improv, comparisons
     uint32_t n, m, nwords;
+    const IrJump* jump;       // generator jump polynomials
     double alpha, beta, tau0, eff_pp, mmf;
     int seeding, coin_always, eta_table;  // eta_table: reference table path (n <= 5000) rounds eta^beta to f32
     double two_opt_prob;
@@ -68,14 +79,45 @@ __device__ __forceinline__ void st_release_cta(volatile uint32_t* p, uint32_t v)
     asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared((const void*)p)), "r"(v) : "memory");
 }
 
-// Draw ring between the generator warp and the construction warp of one ant.
-constexpr uint32_t kIrRing = 2048;          // u64 draws in flight
-constexpr uint32_t kIrCkpt = kIrRing / 32;  // generator states saved every 32 draws
+// Draw ring between the generator warp and the construction warp of one ant. The
+// generator's 32 lanes each produce chunks of kIrChunk consecutive draws of the ant's one
+// stream - lane i chunks i, i + 32, ... - reaching its next chunk with a xoshiro jump
+// (the state advanced by 31 chunks: Cayley-Hamilton, the jump polynomial x^J mod the
+// transition's characteristic polynomial, computed on the host, ir_jump_polys). A round is
+// 32 chunks; the ring holds two rounds.
+constexpr uint32_t kIrChunk = 64;                  // draws per chunk
+constexpr uint32_t kIrRound = 32 * kIrChunk;       // draws per generator round
+constexpr uint32_t kIrRing = 2 * kIrRound;         // u64 draws in flight
+constexpr uint32_t kIrCkpt = kIrRing / kIrChunk;   // chunk start states kept
 struct IrRing {
     unsigned long long draw[kIrRing];
-    unsigned long long ckpt[kIrCkpt][4];    // state before draw 32c (slot c % kIrCkpt)
+    unsigned long long ckpt[kIrCkpt][4];    // state before draw kIrChunk * c (slot c % kIrCkpt)
     volatile uint32_t produced, consumed, stop;
 };
+// ring slot of stream position p: XOR-swizzled inside its chunk, so that the 32 lanes that
+// write one step of their chunks at once fall in different bank pairs
+__device__ __forceinline__ uint32_t ir_slot(uint32_t p) {
+    return ((p & ~(kIrChunk - 1)) | ((p & (kIrChunk - 1)) ^ ((p / kIrChunk) & 15u))) % kIrRing;
+}
+// Jump polynomials (bit b of word w = coefficient of x^(64w+b)): [0..31] lane offsets
+// x^(i * kIrChunk), [32] the step to a lane's next chunk x^(31 * kIrChunk)
+struct IrJump {
+    unsigned long long p[33][4];
+};
+// s <- p(M) s for the xoshiro256 transition M (the structure of the published jump()):
+// the states M^b s accumulated where p has bit b
+__device__ __forceinline__ void xo_jump(uint64_t s[4], const unsigned long long* __restrict__ p) {
+    uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    for (int w = 0; w < 4; ++w) {
+        const uint64_t pw = p[w];
+#pragma unroll 8
+        for (int b = 0; b < 64; ++b) {
+            if ((pw >> b) & 1u) { t0 ^= s[0]; t1 ^= s[1]; t2 ^= s[2]; t3 ^= s[3]; }
+            xoshiro_next(s);
+        }
+    }
+    s[0] = t0; s[1] = t1; s[2] = t2; s[3] = t3;
+}
 
 // One CTA of two warps per ant: detail::build_candidate (engine.hpp:129-148) with
 // construct_full / construct_partial (construction.hpp:283-365) and select_next
@@ -91,52 +133,64 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, ant = blockIdx.x, n = a.n, nw = a.nwords;
     IrRing* ring = reinterpret_cast<IrRing*>(smem_raw);
-    double* acc = reinterpret_cast<double*>(ring + 1);                 // n (P-ACO): ColonyPheromone::acc_
-    double* stage_r = acc + (a.T ? 0 : n);                             // m (P-ACO): this step's ratios
-    uint32_t* stage_c = reinterpret_cast<uint32_t*>(stage_r + (a.T ? 0 : a.m));  // 2m: this step's pairs
-    uint32_t* vis = stage_c + (a.T ? 0 : 2 * a.m);                    // nw
+    double* acc = reinterpret_cast<double*>(ring + 1);  // ir_acc_slots(n) (P-ACO): this step's tau^alpha, negated, at accx(j)
+    uint32_t* vis = reinterpret_cast<uint32_t*>(acc + (a.T ? 0 : ir_acc_slots(n)));  // nw
     if (threadIdx.x == 0) { ring->produced = 0; ring->consumed = 0; ring->stop = 0; }
     if (warp == 0) {
-        if (!a.T) {
-            for (uint32_t j = lane; j < n; j += 32) acc[j] = 0.0;
-            for (uint32_t q = lane; q < a.m; q += 32) stage_r[q] = a.ratio[q];  // fixed for the iteration
+        if (!a.T) {  // untouched cities score with tau0^alpha (ColonyPheromone::mult_, construction.hpp:108-111)
+            const double t0a = power(a.alpha, a.tau0);
+            for (uint32_t j = lane; j < ir_acc_slots(n); j += 32) acc[j] = t0a;
         }
         for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
     }
     __syncthreads();
     if (warp == 1) {
-        if (lane != 0) return;
-        // the generator (rng.hpp:40-50), state carried across iterations in a.rng
+        // the generator warp (rng.hpp:40-50): lane i starts at stream position i * kIrChunk
+        // of the ant's stream (state carried across iterations in a.rng), produces its chunk
+        // of every round, then jumps 31 chunks ahead
         uint64_t s[4];
         for (int q = 0; q < 4; ++q) s[q] = a.rng[(size_t)ant * 4 + q];
-        // batches of 32 draws: the checkpoint, then 32 unrolled steps with no test in
-        // between, so consecutive steps' independent work (the output of one, the state
-        // update of the next) overlaps
-        for (uint32_t p = 0;; p += 32) {
-            if (p - ring->consumed >= kIrRing - 32) {  // keep the consumption checkpoint alive
-                while (p - ring->consumed >= kIrRing - 32 && !ring->stop) __nanosleep(100);
+        if (lane) xo_jump(s, a.jump->p[lane]);
+        for (uint32_t r = 0;; ++r) {
+            // round r reuses round r - 2's slots and checkpoints: wait for them to be consumed
+            if (r >= 2) {
+                if (lane == 0)
+                    while (ld_acquire_cta(&ring->consumed) < (r - 1) * kIrRound && !ring->stop) __nanosleep(64);
+                __syncwarp();
             }
-            if (ring->stop) return;
-            unsigned long long* c = ring->ckpt[(p >> 5) % kIrCkpt];
-            c[0] = s[0]; c[1] = s[1]; c[2] = s[2]; c[3] = s[3];
-            unsigned long long* d = ring->draw + (p % kIrRing);
-#pragma unroll
-            for (int q = 0; q < 32; ++q) d[q] = xoshiro_next(s);
-            st_release_cta(&ring->produced, p + 32);  // the 32 draws before the count
+            // one lane reads the flag, so that the warp leaves the loop together
+            if (__shfl_sync(kFull, lane == 0 ? (uint32_t)ring->stop : 0u, 0)) break;
+            const uint32_t c = 32 * r + lane, p0 = c * kIrChunk;
+            unsigned long long* ck = ring->ckpt[c % kIrCkpt];
+            ck[0] = s[0]; ck[1] = s[1]; ck[2] = s[2]; ck[3] = s[3];
+#pragma unroll 16
+            for (uint32_t q = 0; q < kIrChunk; ++q) ring->draw[ir_slot(p0 + q)] = xoshiro_next(s);
+            xo_jump(s, a.jump->p[32]);
+            __syncwarp();
+            if (lane == 0) st_release_cta(&ring->produced, (r + 1) * kIrRound);  // the round's draws before the count
         }
+        return;
     }
     // ---- warp 0: the construction ----
     if (lane == 0 && (n & 31)) vis[nw - 1] = 0xffffffffu << (n & 31);
     __syncwarp();
     uint32_t cidx = 0;  // draws consumed so far (warp-uniform)
 #ifdef PACO_IRSEG
-    long long sg_wait = 0, sg_begin = 0, sg_scan = 0, sg_end = 0, sg_stage = 0, sg_group = 0;
+    long long sg_wait = 0, sg_begin = 0, sg_scan = 0, sg_end = 0, sg_stage = 0, sg_group = 0, sg_ld = 0, sg_loop = 0;
 #endif
     auto wait_for = [&](uint32_t upto) {  // draws [0, upto) are in the ring
 #ifdef PACO_IRSEG
         const long long w0c = clock64();
 #endif
-        if (lane == 0) while (ld_acquire_cta(&ring->produced) < upto) {}
+        // publish the consumption point first: the generator may be waiting for it to start
+        // the round that holds `upto` (after every lane's reads of the earlier draws: lane 0's
+        // release covers them through the warp barrier)
+        __syncwarp();
+        if (lane == 0) {
+            // a release: the draws read so far are read before the generator may reuse their slots
+            if (ring->consumed != cidx) st_release_cta(&ring->consumed, cidx);
+            while (ld_acquire_cta(&ring->produced) < upto) {}
+        }
         __syncwarp();
 #ifdef PACO_IRSEG
         sg_wait += clock64() - w0c;
@@ -144,7 +198,7 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     };
     auto take = [&]() -> uint64_t {  // next draw, lane 0's view (other lanes follow the index)
         wait_for(cidx + 1);
-        const uint64_t v = ring->draw[cidx % kIrRing];
+        const uint64_t v = ring->draw[ir_slot(cidx)];
         ++cidx;
         return v;
     };
@@ -224,53 +278,12 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
             // (match.any) and the group's lowest lane adds them in lane order, so every acc[c]
             // receives its terms in ant order - the fp64 sum order of the reference.
             if (!a.T) {
-#pragma unroll 4
-                for (uint32_t q = lane; q < a.m; q += 32) {
-                    uint2 pr = make_uint2(kNone, kNone);
-                    if (stage_r[q] != 0.0) pr = a.nbr[(size_t)q * n + cur];
-                    stage_c[2 * q] = pr.x;
-                    stage_c[2 * q + 1] = pr.y;
-                }
-                __syncwarp();
-#ifdef PACO_IRSEG
-                const long long bAc = clock64();
-                sg_stage += bAc - b0c;
-#endif
-                for (uint32_t e0 = 0; e0 < 2 * a.m; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    const uint32_t c = e < 2 * a.m ? stage_c[e] : kNone;
-                    const unsigned live = __ballot_sync(kFull, c != kNone);
-                    if (!live) continue;  // no l_best tour yet (seeding) or no ratio
-                    const unsigned grp = __match_any_sync(kFull, c);
-                    const bool leader = c != kNone && (int)lane == __ffs(grp) - 1;
-                    // each group's leader adds its members' terms in lane order: a serial
-                    // fp64 chain of predicated adds over broadcast loads that do not depend on
-                    // the sum, so the loads are in flight ahead of the chain
-                    double v = leader ? acc[c] : 0.0;
-                    const double* sr = stage_r + (e0 >> 1);
-                    const uint32_t nt = 2 * a.m - e0;  // terms in this pass (may exceed 32)
-#pragma unroll
-                    for (uint32_t src = 0; src < 32; ++src) {
-                        const double x = src < nt ? sr[src >> 1] : 0.0;
-                        if ((grp >> src) & 1u) v = __dadd_rn(v, x);
-                    }
-                    if (leader) acc[c] = v;
-                    __syncwarp();
-                }
-#ifdef PACO_IRSEG
-                sg_group += clock64() - bAc;
-#endif
-                // mult_[c] = Power(alpha)(tau0 + acc[c]) for the touched cities
-                // (construction.hpp:131), stored negated in place of acc[c]: a touched
-                // city's acc is > 0, so the sign tells converted entries apart (lanes that
-                // share a city write the same value)
-                for (uint32_t e = lane; e < 2 * a.m; e += 32) {
-                    const uint32_t c = stage_c[e];
-                    if (c != kNone) {
-                        const double v = acc[c];
-                        if (v > 0.0) acc[c] = -power(a.alpha, __dadd_rn(a.tau0, v));
-                    }
-                }
+                // the step's touched cities and their tau^alpha, precomputed for the iteration
+                // (k_ir_touched); every other city holds tau0^alpha
+                const uint32_t cnt = a.tl_count[cur];
+                const uint32_t* lc = a.tl_city + (size_t)cur * 2 * a.m;
+                const double* lv = a.tl_tau + (size_t)cur * 2 * a.m;
+                for (uint32_t e = lane; e < cnt; e += 32) acc[accx(lc[e])] = lv[e];
                 __syncwarp();
             }
 #ifdef PACO_IRSEG
@@ -282,73 +295,165 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
             double best = -1.0;
             uint32_t bj = kNone;
             uint32_t cnt_total = 0;
-            // one draw per unvisited city in ascending index; four bitmap words per pass so
-            // that four rows of eta / tau loads are in flight per lane
-            constexpr uint32_t U = 4;
-            const unsigned lt = (1u << lane) - 1u;
-            for (uint32_t w0 = 0; w0 < nw; w0 += U) {
-                uint32_t fb[U], cntv[U], tot = 0;
+            if (a.eta_tab && !trow) {
+                // The table path (n <= 5000), P-ACO: words of 32 cities, lane l owning word l of each
+                // chunk of 32 words. A lane's draws are the consecutive block after the unvisited
+                // cities of the lower words (a warp scan of the words' popcounts), its eta^beta
+                // row segment (128 bytes) and tau row segment are loaded at once, and it scores its
+                // unvisited cities in ascending order with strict > (the lowest index keeps a tie).
+                for (uint32_t w0 = 0; w0 < nw; w0 += 32) {
+                    const uint32_t wl = w0 + lane;
+                    const uint32_t fbw = wl < nw ? ~vis[wl] : 0u;
+                    const uint32_t cw = __popc(fbw);
+                    uint32_t incl = cw;
 #pragma unroll
-                for (uint32_t u = 0; u < U; ++u) {
-                    fb[u] = w0 + u < nw ? ~vis[w0 + u] : 0u;
-                    cntv[u] = __popc(fb[u]);
-                    tot += cntv[u];
-                }
-                if (tot == 0) continue;
-                double eta[U], ta[U];
-                if (a.eta_tab) {
-                    // every global load of the pass is issued before the first use (predicated
-                    // PTX loads; left to the compiler, each conversion sat right behind its load
-                    // and a pass made U serial L2 round trips)
-                    const size_t j0 = (size_t)w0 * 32 + lane;
-                    const float* erow = a.eta_tab + (size_t)cur * n + j0;
-                    float ef[U];
-                    double tv[U];
-#pragma unroll
-                    for (uint32_t u = 0; u < U; ++u) {
-                        const bool f = (fb[u] >> lane) & 1u;
-                        ef[u] = ldg_f32_if(erow + u * 32, f);
-                        tv[u] = trow ? ldg_f64_if(trow + j0 + u * 32, f) : (f ? acc[j0 + u * 32] : 0.0);
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= (uint32_t)o) incl += y;
                     }
+                    const uint32_t tot = __shfl_sync(kFull, incl, 31);
+                    if (tot == 0) continue;
+                    const uint32_t excl = incl - cw;
+                    const size_t j0 = (size_t)wl * 32;
+                    float ef[32];
+                    double tv[32];
+                    if (fbw) {
+                        const float4* erow = reinterpret_cast<const float4*>(a.eta_tab + (size_t)cur * n + j0);
+                        // the table's row stride is n: a 16-byte load needs 4-aligned cities
+                        if (((size_t)cur * n + j0) % 4 == 0 && j0 + 32 <= n) {
 #pragma unroll
-                    for (uint32_t u = 0; u < U; ++u) {
-                        eta[u] = (double)ef[u];
-                        ta[u] = trow ? power(a.alpha, tv[u]) : (tv[u] == 0.0 ? tau0_alpha : -tv[u]);
-                    }
-                } else
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 f = erow[q];
+                                ef[4 * q] = f.x; ef[4 * q + 1] = f.y; ef[4 * q + 2] = f.z; ef[4 * q + 3] = f.w;
+                            }
+                        } else {
+                            const float* er = a.eta_tab + (size_t)cur * n + j0;
 #pragma unroll
-                for (uint32_t u = 0; u < U; ++u) {
-                    eta[u] = 0.0; ta[u] = 0.0;
-                    if ((fb[u] >> lane) & 1u) {
-                        const uint32_t j = (w0 + u) * 32 + lane;
-                        {
-                            int32_t d = euc2d(qc, a.xy[j]);
-                            if (d < 1) d = 1;
-                            eta[u] = power(a.beta, 1.0 / (double)d);
-                            if (a.eta_table) eta[u] = (double)(float)eta[u];
+                            for (int q = 0; q < 32; ++q) ef[q] = j0 + q < n ? er[q] : 0.0f;
                         }
-                        if (trow) ta[u] = power(a.alpha, trow[j]);
-                        else {
-                            const double aj = acc[j];
-                            ta[u] = aj == 0.0 ? tau0_alpha : -aj;
-                        }
-                    }
-                }
-                wait_for(cidx + tot);
-                uint32_t off = cidx;
 #pragma unroll
-                for (uint32_t u = 0; u < U; ++u) {
-                    if ((fb[u] >> lane) & 1u) {
-                        const uint64_t raw = ring->draw[(off + __popc(fb[u] & lt)) % kIrRing];
+                        for (int q = 0; q < 32; ++q) tv[q] = ((fbw >> q) & 1u) ? acc[j0 + q + wl] : 0.0;
+                    }
+#ifndef PACO_IRSEG
+                    // the row loads land before the draw wait (left to the compiler they were
+                    // issued behind it: 453 against 373 ms for C1's 100 iterations)
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) asm volatile("" ::"f"(ef[q]), "d"(tv[q]));
+#endif
+#ifdef PACO_IRSEG
+                    const long long q0c = clock64();
+                    double tsum = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) tsum += tv[q] + (double)ef[q];
+                    { long long q1c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(q1c) : "d"(tsum)); sg_ld += q1c - q0c; }
+#endif
+                    wait_for(cidx + tot);
+#ifdef PACO_IRSEG
+                    const long long q2c = clock64();
+#endif
+                    // every city's draw address is its rank among the word's unvisited cities (no
+                    // dependence between cities), and the lane's best is a tree over the 32 cities
+                    // that keeps the lower index on equal scores - the strict > of an ascending scan
+                    const uint32_t base = cidx + excl;
+                    // branch-free: every city is scored (a visited city reads some ring slot and
+                    // gets -1), so the 32 loads, conversions and products overlap
+                    double sc[32];
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const uint64_t raw = ring->draw[ir_slot(base + __popc(fbw & ((1u << q) - 1u)))];
                         const double uu = (double)(raw >> 11) * 0x1.0p-53;
-                        const double score = __dmul_rn(__dmul_rn(ta[u], eta[u]), uu);
-                        if (score > best) { best = score; bj = (w0 + u) * 32 + lane; }
+                        const double v = __dmul_rn(__dmul_rn(tv[q], (double)ef[q]), uu);
+                        sc[q] = ((fbw >> q) & 1u) ? v : -1.0;
                     }
-                    off += cntv[u];
+                    uint32_t ix[32];
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) ix[q] = q;
+#pragma unroll
+                    for (int st = 1; st < 32; st <<= 1) {
+#pragma unroll
+                        for (int q = 0; q + st < 32; q += 2 * st) {
+                            // left (lower index) wins unless right is strictly larger
+                            if (sc[q + st] > sc[q]) { sc[q] = sc[q + st]; ix[q] = ix[q + st]; }
+                        }
+                    }
+                    if (sc[0] > best) { best = sc[0]; bj = (uint32_t)j0 + ix[0]; }
+#ifdef PACO_IRSEG
+                    { long long q3c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(q3c) : "d"(best)); sg_loop += q3c - q2c; }
+#endif
+                    cidx += tot;
+                    cnt_total += tot;
+                    __syncwarp();  // every lane's draws are read before the slots are released
+                    if (lane == 0) st_release_cta(&ring->consumed, cidx);
                 }
-                cidx += tot;
-                cnt_total += tot;
-                if (lane == 0) ring->consumed = cidx;
+            } else {
+                // one draw per unvisited city in ascending index; four bitmap words per pass so
+                // that four rows of eta / tau loads are in flight per lane
+                constexpr uint32_t U = 4;
+                const unsigned lt = (1u << lane) - 1u;
+                for (uint32_t w0 = 0; w0 < nw; w0 += U) {
+                    uint32_t fb[U], cntv[U], tot = 0;
+    #pragma unroll
+                    for (uint32_t u = 0; u < U; ++u) {
+                        fb[u] = w0 + u < nw ? ~vis[w0 + u] : 0u;
+                        cntv[u] = __popc(fb[u]);
+                        tot += cntv[u];
+                    }
+                    if (tot == 0) continue;
+                    double eta[U], ta[U];
+                    if (a.eta_tab) {
+                        // every global load of the pass is issued before the first use (predicated
+                        // PTX loads; left to the compiler, each conversion sat right behind its load
+                        // and a pass made U serial L2 round trips)
+                        const size_t j0 = (size_t)w0 * 32 + lane;
+                        const float* erow = a.eta_tab + (size_t)cur * n + j0;
+                        float ef[U];
+                        double tv[U];
+    #pragma unroll
+                        for (uint32_t u = 0; u < U; ++u) {
+                            const bool f = (fb[u] >> lane) & 1u;
+                            ef[u] = ldg_f32_if(erow + u * 32, f);
+                            tv[u] = trow ? ldg_f64_if(trow + j0 + u * 32, f) : (f ? acc[accx((uint32_t)j0 + u * 32)] : tau0_alpha);
+                        }
+    #pragma unroll
+                        for (uint32_t u = 0; u < U; ++u) {
+                            eta[u] = (double)ef[u];
+                            ta[u] = trow ? power(a.alpha, tv[u]) : tv[u];
+                        }
+                    } else
+    #pragma unroll
+                    for (uint32_t u = 0; u < U; ++u) {
+                        eta[u] = 0.0; ta[u] = 0.0;
+                        if ((fb[u] >> lane) & 1u) {
+                            const uint32_t j = (w0 + u) * 32 + lane;
+                            {
+                                int32_t d = euc2d(qc, a.xy[j]);
+                                if (d < 1) d = 1;
+                                eta[u] = power(a.beta, 1.0 / (double)d);
+                                if (a.eta_table) eta[u] = (double)(float)eta[u];
+                            }
+                            if (trow) ta[u] = power(a.alpha, trow[j]);
+                            else {
+                                ta[u] = acc[accx(j)];
+                            }
+                        }
+                    }
+                    wait_for(cidx + tot);
+                    uint32_t off = cidx;
+    #pragma unroll
+                    for (uint32_t u = 0; u < U; ++u) {
+                        if ((fb[u] >> lane) & 1u) {
+                            const uint64_t raw = ring->draw[ir_slot(off + __popc(fb[u] & lt))];
+                            const double uu = (double)(raw >> 11) * 0x1.0p-53;
+                            const double score = __dmul_rn(__dmul_rn(ta[u], eta[u]), uu);
+                            if (score > best) { best = score; bj = (w0 + u) * 32 + lane; }
+                        }
+                        off += cntv[u];
+                    }
+                    cidx += tot;
+                    cnt_total += tot;
+                    __syncwarp();  // every lane's draws are read before the slots are released
+                    if (lane == 0) st_release_cta(&ring->consumed, cidx);
+                }
             }
             // warp argmax, strict >, lowest city index on equal scores
 #pragma unroll
@@ -364,11 +469,10 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
 #endif
             n_cmp += cnt_total;  // construction.hpp:275
             if (!a.T) {
-                // ColonyPheromone::end_step: reset the touched entries (from the staging list)
-                for (uint32_t e = lane; e < 2 * a.m; e += 32) {
-                    const uint32_t c = stage_c[e];
-                    if (c != kNone) acc[c] = 0.0;
-                }
+                // ColonyPheromone::end_step: reset the touched entries
+                const uint32_t cnt = a.tl_count[cur];
+                const uint32_t* lc = a.tl_city + (size_t)cur * 2 * a.m;
+                for (uint32_t e = lane; e < cnt; e += 32) acc[accx(lc[e])] = tau0_alpha;
                 __syncwarp();
             }
 #ifdef PACO_IRSEG
@@ -386,19 +490,22 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
         atomicAdd(&g_timing[0], (unsigned long long)sg_begin); atomicAdd(&g_timing[1], (unsigned long long)sg_scan);
         atomicAdd(&g_timing[2], (unsigned long long)sg_wait); atomicAdd(&g_timing[3], (unsigned long long)sg_end);
         atomicAdd(&g_timing[4], n_dec); atomicAdd(&g_timing[5], n_cmp);
-        atomicAdd(&g_timing[6], (unsigned long long)sg_stage); atomicAdd(&g_timing[7], (unsigned long long)sg_group);
+        atomicAdd(&g_timing[6], (unsigned long long)sg_ld); atomicAdd(&g_timing[7], (unsigned long long)sg_loop);
     }
 #endif
     // maybe_two_opt consumes exactly one draw (two_opt.hpp:71-76)
     const uint32_t do2 = uniform() < a.two_opt_prob ? 1u : 0u;
-    // stop the generator; the stream state after exactly cidx draws: the checkpoint at
-    // cidx rounded down to 32 (still alive, see above) advanced by the remainder
+    // stop the generator; the stream state after exactly cidx draws: the start state of the
+    // chunk holding position cidx (alive: the generator never runs two rounds past the
+    // consumption point) advanced by the remainder
+    wait_for(cidx + 1);  // the chunk holding position cidx is produced: its start state is kept
+    __syncwarp();
     if (lane == 0) {
-        ring->consumed = cidx;
+        st_release_cta(&ring->consumed, cidx);
         ring->stop = 1;
-        const unsigned long long* c = ring->ckpt[(cidx >> 5) % kIrCkpt];
+        const unsigned long long* c = ring->ckpt[(cidx / kIrChunk) % kIrCkpt];
         uint64_t s[4] = {c[0], c[1], c[2], c[3]};
-        for (uint32_t q = 0; q < (cidx & 31u); ++q) xoshiro_next(s);
+        for (uint32_t q = 0; q < cidx % kIrChunk; ++q) xoshiro_next(s);
         for (int q = 0; q < 4; ++q) a.rng[(size_t)ant * 4 + q] = s[q];
     }
     __syncwarp();
@@ -412,6 +519,79 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
         atomicAdd(&a.counters[partial ? 5 : 4], 1ull);
         atomicAdd(&a.counters[8], n_cmp);
         if (do2) atomicAdd(&a.counters[9], 1ull);
+    }
+}
+
+// ColonyPheromone::begin_step (construction.hpp:121-132) of every city, once per synchronous
+// iteration: the colony is frozen for the iteration (engine.hpp:246-248), so the touched
+// cities of a step at city c and their tau^alpha = Power(alpha)(tau0 + acc) are the same for
+// every ant and every decision at c. One warp per city: the 2m contributions (ant q's prev
+// then next of c, skipped when ratio q is 0) are staged, then applied 32 per pass - lanes that
+// hit the same city are grouped (match.any) and the group's lowest lane adds them in lane
+// order, so every acc receives its terms in ant order, the reference's fp64 sum order. The
+// list of (touched city, tau^alpha) is written in first-occurrence order.
+__global__ void __launch_bounds__(32) k_ir_touched(const uint2* __restrict__ nbr, const double* __restrict__ ratio,
+                                                   uint32_t n, uint32_t m, double alpha, double tau0,
+                                                   uint32_t* __restrict__ tl_city, double* __restrict__ tl_tau,
+                                                   uint32_t* __restrict__ tl_count) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* acc = reinterpret_cast<double*>(smem_raw);   // n
+    double* stage_r = acc + n;                           // m
+    uint32_t* stage_c = reinterpret_cast<uint32_t*>(stage_r + m);  // 2m
+    const uint32_t lane = threadIdx.x;
+    for (uint32_t j = lane; j < n; j += 32) acc[j] = 0.0;
+    for (uint32_t q = lane; q < m; q += 32) stage_r[q] = ratio[q];
+    __syncwarp();
+    for (uint32_t c = blockIdx.x; c < n; c += gridDim.x) {
+        for (uint32_t q = lane; q < m; q += 32) {
+            uint2 pr = make_uint2(kNone, kNone);
+            if (stage_r[q] != 0.0) pr = nbr[(size_t)q * n + c];
+            stage_c[2 * q] = pr.x;
+            stage_c[2 * q + 1] = pr.y;
+        }
+        __syncwarp();
+        for (uint32_t e0 = 0; e0 < 2 * m; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            const uint32_t cc = e < 2 * m ? stage_c[e] : kNone;
+            const unsigned live = __ballot_sync(kFull, cc != kNone);
+            if (!live) continue;
+            const unsigned grp = __match_any_sync(kFull, cc);
+            const bool leader = cc != kNone && (int)lane == __ffs(grp) - 1;
+            double v = leader ? acc[cc] : 0.0;
+            const double* sr = stage_r + (e0 >> 1);
+            const uint32_t nt = 2 * m - e0;
+#pragma unroll
+            for (uint32_t src = 0; src < 32; ++src) {
+                const double x = src < nt ? sr[src >> 1] : 0.0;
+                if ((grp >> src) & 1u) v = __dadd_rn(v, x);
+            }
+            if (leader) acc[cc] = v;
+            __syncwarp();
+        }
+        // the list: each touched city once (its first occurrence), tau^alpha, then acc reset
+        uint32_t cnt = 0;
+        uint32_t* oc = tl_city + (size_t)c * 2 * m;
+        double* ov = tl_tau + (size_t)c * 2 * m;
+        for (uint32_t e0 = 0; e0 < 2 * m; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            const uint32_t cc = e < 2 * m ? stage_c[e] : kNone;
+            const unsigned grp = __match_any_sync(kFull, cc);
+            const bool first_here = cc != kNone && (int)lane == __ffs(grp) - 1;
+            // a city already listed by an earlier pass has acc reset to 0 (acc > 0 otherwise)
+            const double a = first_here ? acc[cc] : 0.0;
+            const bool emit = first_here && a > 0.0;
+            const unsigned ball = __ballot_sync(kFull, emit);
+            if (emit) {
+                const uint32_t slot = cnt + __popc(ball & ((1u << lane) - 1u));
+                oc[slot] = cc;
+                ov[slot] = power(alpha, __dadd_rn(tau0, a));
+                acc[cc] = 0.0;
+            }
+            cnt += __popc(ball);
+            __syncwarp();
+        }
+        if (lane == 0) tl_count[c] = cnt;
+        __syncwarp();
     }
 }
 

@@ -10,6 +10,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -142,6 +143,10 @@ struct paco_handle {
     bool ir = false;
     uint64_t* rng = nullptr;   // m*4 xoshiro256++ states
     double* ratio = nullptr;   // m
+    uint32_t* tl_city = nullptr;   // reference rule, P-ACO: n*2m touched cities per begin_step (k_ir_touched)
+    double* tl_tau = nullptr;      // n*2m their tau^alpha
+    uint32_t* tl_count = nullptr;  // n
+    IrJump* ir_jump = nullptr;     // reference rule: the generator's jump polynomials
     double* Tfull = nullptr;   // classic: n*n
     float* eta_tab = nullptr;  // n*n eta^beta f32 (n <= 5000)
 
@@ -151,7 +156,7 @@ struct paco_handle {
         if (st2) cudaStreamSynchronize(st2);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
                         partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words, order, two_opt_flag, two_opt_edges, two_opt_txy,
-                        scratch_u32, scratch_u64, rng, ratio, Tfull, eta_tab, cand_mult};
+                        scratch_u32, scratch_u64, rng, ratio, tl_city, tl_tau, tl_count, ir_jump, Tfull, eta_tab, cand_mult};
         for (void* p : ptrs) dfree(p);
         for (auto e : evpool) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
@@ -284,8 +289,11 @@ static paco_status build_grid(paco_handle* h) {
 }
 
 // reference rule: [draw ring] [acc n doubles (P-ACO)] [bitmap]
+// k_ir_touched: acc[n] (fp64) | ratios[m] (fp64) | the step's 2m contributions (u32)
+static size_t ir_touched_smem(uint32_t n, uint32_t m) { return (size_t)8 * n + (size_t)8 * m + (size_t)8 * m; }
 static size_t ir_smem_bytes(uint32_t n, uint32_t m, uint32_t nwords, int mode) {
-    return sizeof(IrRing) + (mode == PACO_MODE_CLASSIC ? 0 : (size_t)8 * n + (size_t)16 * m) + (size_t)nwords * 4;
+    (void)m;
+    return sizeof(IrRing) + (mode == PACO_MODE_CLASSIC ? 0 : (size_t)8 * ir_acc_slots(n)) + (size_t)nwords * 4;
 }
 
 // colony state shared by both selection rules
@@ -392,6 +400,103 @@ static void rng_for_stream(uint64_t master, uint64_t stream, uint64_t out[4]) {
     for (int q = 0; q < 4; ++q) out[q] = splitmix_next(seed);
 }
 
+// ---- xoshiro256 jump polynomials (the reference-rule generator, kernels_ir.cuh) ----
+// The state update of xoshiro256++ (rng.hpp:40-50) is linear over GF(2)^256; by
+// Cayley-Hamilton, advancing J steps is p(M) with p = x^J mod P, P the characteristic
+// polynomial of M. P is the minimal polynomial of a state-bit sequence (Berlekamp-Massey;
+// degree 256), x^J mod P by square-and-multiply.
+using Poly = std::array<uint64_t, 8>;  // up to degree 511
+static void xo_host_step(uint64_t s[4]) {
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t;
+    s[3] = (s[3] << 45) | (s[3] >> 19);
+}
+static bool pbit(const Poly& a, int i) { return (a[i >> 6] >> (i & 63)) & 1u; }
+static void pflip(Poly& a, int i) { a[i >> 6] ^= 1ull << (i & 63); }
+static bool xo_char_poly(Poly& P) {
+    // the sequence: bit 0 of s[0] along the orbit of a fixed nonzero state
+    uint64_t s[4] = {0x9e3779b97f4a7c15ull, 0xbf58476d1ce4e5b9ull, 0x94d049bb133111ebull, 0x2545f4914f6cdd1dull};
+    const int N = 1024;
+    std::vector<uint8_t> seq(N);
+    for (int i = 0; i < N; ++i) { seq[i] = (uint8_t)(s[0] & 1u); xo_host_step(s); }
+    std::vector<uint8_t> C(N + 1, 0), B(N + 1, 0), T;
+    C[0] = B[0] = 1;
+    int L = 0, m = 1;
+    for (int n = 0; n < N; ++n) {
+        uint8_t d = seq[n];
+        for (int i = 1; i <= L; ++i) d ^= (uint8_t)(C[i] & seq[n - i]);
+        if (!d) { ++m; continue; }
+        T = C;
+        for (int i = 0; i + m <= N; ++i) C[i + m] ^= B[i];
+        if (2 * L <= n) { L = n + 1 - L; B = T; m = 1; } else ++m;
+    }
+    if (L != 256) return false;
+    P.fill(0);
+    for (int k = 0; k <= L; ++k) if (C[L - k]) pflip(P, k);  // reciprocal of the connection polynomial
+    return true;
+}
+static Poly pmulmod(const Poly& a, const Poly& b, const Poly& P) {
+    Poly r{};
+    for (int i = 0; i < 256; ++i)
+        if (pbit(a, i))
+            for (int j = 0; j < 256; ++j) if (pbit(b, j)) pflip(r, i + j);
+    for (int k = 510; k >= 256; --k)
+        if (pbit(r, k))
+            for (int j = 0; j <= 256; ++j) if (pbit(P, j)) pflip(r, k - 256 + j);
+    return r;
+}
+static Poly pxpow(uint64_t J, const Poly& P) {  // x^J mod P
+    Poly r{}; r[0] = 1;
+    for (int b = 63; b >= 0; --b) {
+        r = pmulmod(r, r, P);
+        if ((J >> b) & 1u) {  // multiply by x
+            Poly t{};
+            for (int i = 0; i < 256; ++i) if (pbit(r, i)) pflip(t, i + 1);
+            if (pbit(t, 256)) for (int j = 0; j <= 256; ++j) if (pbit(P, j)) pflip(t, j);
+            r = t;
+        }
+    }
+    return r;
+}
+static void xo_host_jump(uint64_t s[4], const Poly& p) {
+    uint64_t t[4] = {0, 0, 0, 0};
+    for (int b = 0; b < 256; ++b) {
+        if (pbit(p, b)) for (int q = 0; q < 4; ++q) t[q] ^= s[q];
+        xo_host_step(s);
+    }
+    for (int q = 0; q < 4; ++q) s[q] = t[q];
+}
+// the table the generator uses, checked against direct stepping once per process
+static bool ir_jump_table(IrJump& J) {
+    static std::mutex mu;
+    static bool done = false, ok = false;
+    static IrJump cached;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done) {
+        done = true;
+        Poly P;
+        if (xo_char_poly(P)) {
+            for (uint32_t i = 0; i < 33; ++i) {
+                const Poly q = pxpow(i < 32 ? (uint64_t)i * kIrChunk : 31ull * kIrChunk, P);
+                for (int w = 0; w < 4; ++w) cached.p[i][w] = q[w];
+            }
+            ok = true;
+            for (uint32_t i : {1u, 7u, 31u, 32u}) {
+                uint64_t a[4] = {1, 2, 3, 0xdeadbeefcafef00dull}, b[4];
+                std::memcpy(b, a, sizeof a);
+                Poly q{};
+                for (int w = 0; w < 4; ++w) q[w] = cached.p[i][w];
+                xo_host_jump(a, q);
+                const uint64_t steps = i < 32 ? (uint64_t)i * kIrChunk : 31ull * kIrChunk;
+                for (uint64_t k = 0; k < steps; ++k) xo_host_step(b);
+                ok = ok && std::memcmp(a, b, sizeof a) == 0;
+            }
+        }
+    }
+    J = cached;
+    return ok;
+}
+
 // Reference-rule mode: cities stay in their original order (the rule consumes draws
 // in ascending city index), no candidate lists.
 static paco_status setup_ir(paco_handle* h) {
@@ -414,6 +519,18 @@ static paco_status setup_ir(paco_handle* h) {
     CU(cudaMemcpyAsync(h->rng, st.data(), sizeof(uint64_t) * st.size(), cudaMemcpyHostToDevice, h->st));
     CU(dalloc(&h->ratio, m));
     CU(cudaMemsetAsync(h->ratio, 0, sizeof(double) * m, h->st));
+    {
+        IrJump J;
+        if (!ir_jump_table(J)) return fail(PACO_E_RUNTIME, "xoshiro256 jump polynomials failed their self-check");
+        CU(dalloc(&h->ir_jump, 1));
+        CU(cudaMemcpyAsync(h->ir_jump, &J, sizeof J, cudaMemcpyHostToDevice, h->st));
+        CU(cudaStreamSynchronize(h->st));  // before J goes out of scope
+    }
+    if (h->mode != PACO_MODE_CLASSIC) {
+        CU(dalloc(&h->tl_city, (size_t)n * 2 * m));
+        CU(dalloc(&h->tl_tau, (size_t)n * 2 * m));
+        CU(dalloc(&h->tl_count, n));
+    }
     if (n <= 5000) {  // the reference keeps eta^beta in an f32 table for these sizes
         CU(dalloc(&h->eta_tab, (size_t)n * n));
         k_eta_table<<<(unsigned)(((size_t)n * n + 255) / 256), 256, 0, h->st>>>(h->xy, n, h->cfg.beta, h->eta_tab);
@@ -545,6 +662,8 @@ paco_status paco_create(const double* xs, const double* ys, uint32_t n, const pa
     if (ir) {
         if (ir_smem_bytes(n, cfg->ants, nwords, mode) + static_smem((const void*)k_construct_ir) > optin)
             return fail(PACO_E_UNSUPPORTED, "reference-rule per-ant state exceeds shared memory (n too large)");
+        if (mode != PACO_MODE_CLASSIC && ir_touched_smem(n, cfg->ants) > optin)
+            return fail(PACO_E_UNSUPPORTED, "reference-rule pheromone staging exceeds shared memory (n or ants too large)");
     } else {
         if (construct_smem_need(kpp, nwords, want_async) > optin)
             return fail(PACO_E_UNSUPPORTED, "visited bitmap exceeds shared memory (n too large)");
@@ -627,6 +746,13 @@ static paco_status launch_weights(paco_handle* h, cudaStream_t stream = nullptr,
 static paco_status launch_ratios(paco_handle* h) {
     if (h->mode == PACO_MODE_CLASSIC) return PACO_OK;
     k_ratios<<<(h->m + 127) / 128, 128, 0, h->st>>>(h->lb_len, h->has_lb, h->g_len, h->m, h->ratio);
+    // every city's begin_step for the iteration (the colony is frozen until the completion step)
+    const size_t smem = ir_touched_smem(h->n, h->m);
+    if (smem > 48 * 1024)
+        CU(cudaFuncSetAttribute(k_ir_touched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint32_t grid = std::min<uint32_t>(h->n, 8 * (uint32_t)h->num_sms);
+    k_ir_touched<<<grid, 32, smem, h->st>>>(h->nbr, h->ratio, h->n, h->m, h->cfg.alpha, h->cfg.tau0, h->tl_city,
+                                            h->tl_tau, h->tl_count);
     CU(cudaGetLastError());
     return PACO_OK;
 }
@@ -634,6 +760,8 @@ static paco_status launch_ratios(paco_handle* h) {
 static paco_status launch_construct_ir(paco_handle* h, bool seeding) {
     IrArgs a{};
     a.xy = h->xy; a.nbr = h->nbr; a.ratio = h->ratio;
+    a.tl_city = h->tl_city; a.tl_tau = h->tl_tau; a.tl_count = h->tl_count;
+    a.jump = h->ir_jump;
     a.T = h->mode == PACO_MODE_CLASSIC ? h->Tfull : nullptr;
     a.rng = h->rng; a.tours = h->tours; a.lb_sel = h->lb_sel; a.new_len = h->new_len;
     a.partial_flag = h->partial; a.counters = h->counters;
