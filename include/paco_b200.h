@@ -117,6 +117,11 @@ int paco_version(void);
 /* Device memory of destroyed handles stays cached in the device's stream-ordered pool for
  * the next handle; this returns it to the driver (device < 0: the current device). */
 paco_status paco_release_cached_memory(int device);
+/* Advance a xoshiro256++ state (rng.hpp:40-50; the reference's per-ant stream, Rng::for_stream)
+ * by `steps` draws with a jump polynomial (x^steps mod the transition's characteristic
+ * polynomial) - the jump the reference-rule generator's lanes use. Host-only arithmetic, no
+ * device; fails if the characteristic polynomial cannot be found. */
+paco_status paco_rng_jump(const uint64_t state_in[4], uint64_t steps, uint64_t state_out[4]);
 
 /* defaults of RunConfig (engine.hpp:42-59) except synchronous = 1 (deterministic per
  * seed; the reference defaults to asynchronous), plus candidates = 16 */

@@ -30,7 +30,7 @@ EXPORTED = (
     "paco_destroy", "paco_iterate", "paco_set_draws", "paco_get_tours", "paco_get_l_best",
     "paco_get_g_best", "paco_get_counters", "paco_get_build_flags", "paco_get_candidates",
     "paco_get_timing", "paco_offer_tour", "paco_construct_at", "paco_run", "paco_run_traced",
-    "paco_release_cached_memory",
+    "paco_release_cached_memory", "paco_rng_jump",
 )
 
 
@@ -97,6 +97,7 @@ def load() -> ctypes.CDLL:
         "paco_last_error": (c_char_p, []),
         "paco_version": (c_int, []),
         "paco_release_cached_memory": (c_int, [c_int]),
+        "paco_rng_jump": (c_int, [P(ctypes.c_uint64), ctypes.c_uint64, P(ctypes.c_uint64)]),
         "paco_config_default": (c_int, [P(Config)]),
         "paco_config_validate": (c_int, [P(Config), c_uint32, c_int]),
         "paco_create": (c_int, [P(c_double), P(c_double), c_uint32, P(Config), c_int, P(vp)]),

@@ -497,6 +497,23 @@ static bool ir_jump_table(IrJump& J) {
     return ok;
 }
 
+// C ABI (declared extern "C" in paco_b200.h)
+paco_status paco_rng_jump(const uint64_t state_in[4], uint64_t steps, uint64_t state_out[4]) {
+    if (!state_in || !state_out) return fail(PACO_E_INVALID, "null state");
+    static std::mutex mu;
+    static bool have = false;
+    static Poly P;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!have) have = xo_char_poly(P);
+        if (!have) return fail(PACO_E_RUNTIME, "xoshiro256 characteristic polynomial not found");
+    }
+    uint64_t s[4] = {state_in[0], state_in[1], state_in[2], state_in[3]};
+    xo_host_jump(s, pxpow(steps, P));
+    for (int q = 0; q < 4; ++q) state_out[q] = s[q];
+    return PACO_OK;
+}
+
 // Reference-rule mode: cities stay in their original order (the rule consumes draws
 // in ascending city index), no candidate lists.
 static paco_status setup_ir(paco_handle* h) {

@@ -253,3 +253,28 @@ def test_cpp_drop_in_header_compiles_and_fails_loudly_without_gpu(native, tmp_pa
     out = subprocess.run([exe, "0"], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
     assert "no GPU" in out.stdout
+
+
+def test_rng_jump_matches_stepping(native):
+    """paco_rng_jump (the reference-rule generator's jump: x^J mod the characteristic polynomial
+    of the xoshiro256 transition, Cayley-Hamilton) equals J single steps of rng.hpp:40-50."""
+    import ctypes
+
+    M = (1 << 64) - 1
+
+    def step(s):
+        s = list(s)
+        t = (s[1] << 17) & M
+        s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t
+        s[3] = ((s[3] << 45) | (s[3] >> 19)) & M
+        return s
+
+    for state, steps in (([1, 2, 3, 4], 0), ([1, 2, 3, 4], 1), ([0x9E3779B97F4A7C15, 7, 0, 12345], 64),
+                         ([5, 6, 7, 8], 31 * 64), ([11, 22, 33, 44], 12345)):
+        inp = (ctypes.c_uint64 * 4)(*state)
+        out = (ctypes.c_uint64 * 4)()
+        assert native.paco_rng_jump(inp, steps, out) == 0
+        ref = state
+        for _ in range(steps):
+            ref = step(ref)
+        assert list(out) == ref, (state, steps)
