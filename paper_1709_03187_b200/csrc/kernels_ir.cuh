@@ -356,13 +356,15 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
                     // that keeps the lower index on equal scores - the strict > of an ascending scan
                     const uint32_t base = cidx + excl;
                     // branch-free: every city is scored (a visited city reads some ring slot and
-                    // gets -1), so the 32 loads, conversions and products overlap
+                    // gets -1), so the 32 loads, conversions and products overlap. The score is
+                    // taken times 2^53: (tau * eta) * ((raw >> 11) * 2^-53) rounds like
+                    // (tau * eta) * (raw >> 11) scaled by the exact power of two, so the order of
+                    // the scores - all the argmax uses - is the reference's
                     double sc[32];
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
                         const uint64_t raw = ring->draw[ir_slot(base + __popc(fbw & ((1u << q) - 1u)))];
-                        const double uu = (double)(raw >> 11) * 0x1.0p-53;
-                        const double v = __dmul_rn(__dmul_rn(tv[q], (double)ef[q]), uu);
+                        const double v = __dmul_rn(__dmul_rn(tv[q], (double)ef[q]), (double)(raw >> 11));
                         sc[q] = ((fbw >> q) & 1u) ? v : -1.0;
                     }
                     uint32_t ix[32];
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
                             if (sc[q + st] > sc[q]) { sc[q] = sc[q + st]; ix[q] = ix[q + st]; }
                         }
                     }
-                    if (sc[0] > best) { best = sc[0]; bj = (uint32_t)j0 + ix[0]; }
+                    if (sc[0] > best) { best = sc[0]; bj = (uint32_t)j0 + ix[0]; }  // best is scaled by 2^53 here
 #ifdef PACO_IRSEG
                     { long long q3c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(q3c) : "d"(best)); sg_loop += q3c - q2c; }
 #endif
