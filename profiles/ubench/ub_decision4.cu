@@ -23,7 +23,7 @@
 #include "device.cuh"
 using namespace pacob200;
 
-enum : int { BASE = 0, ROW2 = 1, ROW1 = 2, ROWI = 4, NOWARM = 8, TM = 16, WLDG = 32 };
+enum : int { BASE = 0, ROW2 = 1, ROW1 = 2, ROWI = 4, NOWARM = 8, TM = 16, WLDG = 32, WPF = 64, WPF2 = 128 };
 __device__ __forceinline__ uint32_t ldg_ca_u32_if(const void* p, bool cond) {
     uint32_t v = 0;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.ca.u32 %0, [%1];\n\t}" : "+r"(v) : "l"(p), "r"((uint32_t)cond));
@@ -161,6 +161,15 @@ __global__ void __launch_bounds__(32, 1) dec(const uint2* __restrict__ cand, con
                                                  : reinterpret_cast<const unsigned char*>(cand + (size_t)e.x * 16);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) wd[c] = ldg_ca_u32_if(src + 32 * c, fe);
+            } else if (V & (WPF | WPF2)) {
+                const unsigned char* src = SPLIT ? reinterpret_cast<const unsigned char*>(split + (size_t)e.x * 32)
+                                                 : reinterpret_cast<const unsigned char*>(cand + (size_t)e.x * 16);
+                if (fe) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(src + 32 * c));
+                    }
+                }
             } else if (!(V & NOWARM)) {
                 const unsigned char* src = SPLIT ? reinterpret_cast<const unsigned char*>(split + (size_t)e.x * 32)
                                                  : reinterpret_cast<const unsigned char*>(cand + (size_t)e.x * 16);
@@ -450,6 +459,11 @@ int main() {
     run<BASE | TM | WLDG>("base ldg-warm timed", cand, split, n, D, 1, tours, cyc, seg, true);
     run<BASE | TM>("base timed", cand, split, n, D, 1024, tours, cyc, seg, true);
     run<BASE | TM | WLDG>("base ldg-warm timed", cand, split, n, D, 1024, tours, cyc, seg, false);
+    for (uint32_t mm : {1024u, 148u, 1u}) {
+        run<BASE>("base (engine loop)", cand, split, n, D, mm, tours, cyc, seg, true);
+        run<BASE | WPF>("base prefetch.L1 warm", cand, split, n, D, mm, tours, cyc, seg, false);
+        run<BASE | NOWARM>("base no warm", cand, split, n, D, mm, tours, cyc, seg, false);
+    }
     for (uint32_t mm : {1024u, 444u, 148u, 1u}) {
         run<BASE>("base (engine loop)", cand, split, n, D, mm, tours, cyc, seg, true);
         run<BASE | WLDG>("base ldg-warm", cand, split, n, D, mm, tours, cyc, seg, false);
