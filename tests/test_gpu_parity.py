@@ -180,6 +180,19 @@ def test_tiny_instances(n, k):
     lockstep(inst, 6, ants=3, candidates=k, seed=n)
 
 
+@pytest.mark.parametrize("path", ["cta", "cluster"])
+@pytest.mark.parametrize("n,w2", [(4, 0), (5, 1), (6, 2), (33, 0), (33, 3), (64, 63)])
+def test_two_opt_tiny_instances(n, w2, path, monkeypatch):
+    """2-opt on every construction of tiny tours (windows 0 = unbounded, 1, 2, 3, n - 1) through
+    both synchronous search kernels: the cluster's ring, rounds and move records at the edges
+    (the (0, n - 1) pair excluded, the closing edge, windows wider than the tour) against O2."""
+    monkeypatch.setenv("PACO_TWO_OPT_PATH", path)
+    rng = np.random.default_rng(100 + n)
+    inst = Instance("tiny2", rng.integers(0, 1000, n).astype(float), rng.integers(0, 1000, n).astype(float))
+    col, ref = lockstep(inst, 5, ants=4, candidates=min(8, n - 1), seed=n + w2, two_opt_prob=1.0, two_opt_window=w2)
+    assert col.counters()["two_opts"] == ref.counters()["two_opts"] > 0
+
+
 @pytest.mark.parametrize("n,k", [(300, 1), (300, 2), (500, 32), (2000, 7), (1500, 15), (1500, 19)])
 def test_candidate_counts(n, k):
     """Every scan template: k = 15/16 (KP 16), 19/20 (KP 20) and the runtime-k path (k = 1, 2,
