@@ -369,7 +369,9 @@ def run_ours(args, rank, world, local):
         "async": {"value": a_dec / (a_ms / 1e3), "unit": UNIT, "iterations": spec["iterations"] - 1,
                   "ms": a_ms, "note": "synchronous=False (engine.hpp:213-244): one barrier-free launch for the "
                                       "config's iteration budget after seeding; weights rebuilt concurrently"},
-        "gpu_launches": 4 * args.steps,
+        # per synchronous partial-mode step: k_weights, k_ant_order (longest ants first),
+        # k_construct, k_update, k_publish (profiles/r02_launches_c5.csv)
+        "gpu_launches": 5 * args.steps,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
