@@ -50,9 +50,9 @@ struct IrArgs {
     const double2* xy;        // original order
     const uint2* nbr;         // m*n (prev, next) of each ant's l_best (P-ACO)
     const double* ratio;      // m g/l ratios snapshotted for this iteration (0 = no tour)
-    const uint32_t* tl_city;  // P-ACO: n*2m touched cities of each city's begin_step (k_ir_touched)
+    const uint32_t* tl_city;  // P-ACO: n rows of 2m + 1: the count, then the touched cities of each
+                              // city's begin_step (k_ir_touched)
     const double* tl_tau;     // n*2m their tau^alpha
-    const uint32_t* tl_count; // n
     const double* T;          // classic: n*n pheromone matrix, else nullptr
     const float* eta_tab;     // n*n eta^beta as f32 (the reference's table path, n <= 5000), else nullptr
     uint64_t* rng;            // m*4 xoshiro256++ states, carried across iterations
@@ -252,6 +252,9 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
     // full constructions score every step (the last one with a single candidate);
     // partial constructions append the final city unscored (construction.hpp:338-348)
     const uint32_t scored = partial ? (remaining > 0 ? remaining - 1 : 0) : remaining;
+    const uint32_t* lc = nullptr;  // the current step's touched-city list (P-ACO)
+    const double* lv = nullptr;
+    uint32_t tl0 = 0u, tl_cnt = 0u;  // this lane's first-round slot, the list's length
     for (uint32_t step = 0; step < remaining; ++step) {
         uint32_t next;
         if (step >= scored) {
@@ -280,10 +283,15 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
             if (!a.T) {
                 // the step's touched cities and their tau^alpha, precomputed for the iteration
                 // (k_ir_touched); every other city holds tau0^alpha
-                const uint32_t cnt = a.tl_count[cur];
-                const uint32_t* lc = a.tl_city + (size_t)cur * 2 * a.m;
-                const double* lv = a.tl_tau + (size_t)cur * 2 * a.m;
-                for (uint32_t e = lane; e < cnt; e += 32) acc[accx(lc[e])] = lv[e];
+                // (k_ir_touched); every other city holds tau0^alpha. One round trip for the count
+                // (lane 0) and the first 31 entries (lanes 1..31); longer lists loop.
+                lc = a.tl_city + (size_t)cur * (2 * a.m + 1);
+                lv = a.tl_tau + (size_t)cur * 2 * a.m;
+                tl0 = lane <= 2 * a.m ? lc[lane] : 0u;
+                const double v0 = lane >= 1 && lane <= 2 * a.m ? lv[lane - 1] : 0.0;
+                tl_cnt = __shfl_sync(kFull, tl0, 0);
+                if (lane >= 1 && lane <= tl_cnt) acc[accx(tl0)] = v0;
+                for (uint32_t e = 31 + lane; e < tl_cnt; e += 32) acc[accx(lc[e + 1])] = lv[e];
                 __syncwarp();
             }
 #ifdef PACO_IRSEG
@@ -472,9 +480,8 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
             n_cmp += cnt_total;  // construction.hpp:275
             if (!a.T) {
                 // ColonyPheromone::end_step: reset the touched entries
-                const uint32_t cnt = a.tl_count[cur];
-                const uint32_t* lc = a.tl_city + (size_t)cur * 2 * a.m;
-                for (uint32_t e = lane; e < cnt; e += 32) acc[accx(lc[e])] = tau0_alpha;
+                if (lane >= 1 && lane <= tl_cnt) acc[accx(tl0)] = tau0_alpha;
+                for (uint32_t e = 31 + lane; e < tl_cnt; e += 32) acc[accx(lc[e + 1])] = tau0_alpha;
                 __syncwarp();
             }
 #ifdef PACO_IRSEG
@@ -534,8 +541,7 @@ __global__ void __launch_bounds__(64, 1) k_construct_ir(IrArgs a) {
 // list of (touched city, tau^alpha) is written in first-occurrence order.
 __global__ void __launch_bounds__(32) k_ir_touched(const uint2* __restrict__ nbr, const double* __restrict__ ratio,
                                                    uint32_t n, uint32_t m, double alpha, double tau0,
-                                                   uint32_t* __restrict__ tl_city, double* __restrict__ tl_tau,
-                                                   uint32_t* __restrict__ tl_count) {
+                                                   uint32_t* __restrict__ tl_city, double* __restrict__ tl_tau) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* acc = reinterpret_cast<double*>(smem_raw);   // n
     double* stage_r = acc + n;                           // m
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(32) k_ir_touched(const uint2* __restrict__ nbr
         }
         // the list: each touched city once (its first occurrence), tau^alpha, then acc reset
         uint32_t cnt = 0;
-        uint32_t* oc = tl_city + (size_t)c * 2 * m;
+        uint32_t* oc = tl_city + (size_t)c * (2 * m + 1) + 1;  // slot 0: the count
         double* ov = tl_tau + (size_t)c * 2 * m;
         for (uint32_t e0 = 0; e0 < 2 * m; e0 += 32) {
             const uint32_t e = e0 + lane;
@@ -592,7 +598,7 @@ __global__ void __launch_bounds__(32) k_ir_touched(const uint2* __restrict__ nbr
             cnt += __popc(ball);
             __syncwarp();
         }
-        if (lane == 0) tl_count[c] = cnt;
+        if (lane == 0) oc[-1] = cnt;
         __syncwarp();
     }
 }

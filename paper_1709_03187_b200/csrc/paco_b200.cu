@@ -143,9 +143,8 @@ struct paco_handle {
     bool ir = false;
     uint64_t* rng = nullptr;   // m*4 xoshiro256++ states
     double* ratio = nullptr;   // m
-    uint32_t* tl_city = nullptr;   // reference rule, P-ACO: n*2m touched cities per begin_step (k_ir_touched)
+    uint32_t* tl_city = nullptr;   // reference rule, P-ACO: n rows of 2m + 1 (count, touched cities; k_ir_touched)
     double* tl_tau = nullptr;      // n*2m their tau^alpha
-    uint32_t* tl_count = nullptr;  // n
     IrJump* ir_jump = nullptr;     // reference rule: the generator's jump polynomials
     double* Tfull = nullptr;   // classic: n*n
     float* eta_tab = nullptr;  // n*n eta^beta f32 (n <= 5000)
@@ -156,7 +155,7 @@ struct paco_handle {
         if (st2) cudaStreamSynchronize(st2);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
                         partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words, order, two_opt_flag, two_opt_edges, two_opt_txy,
-                        scratch_u32, scratch_u64, rng, ratio, tl_city, tl_tau, tl_count, ir_jump, Tfull, eta_tab, cand_mult};
+                        scratch_u32, scratch_u64, rng, ratio, tl_city, tl_tau, ir_jump, Tfull, eta_tab, cand_mult};
         for (void* p : ptrs) dfree(p);
         for (auto e : evpool) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
@@ -544,9 +543,8 @@ static paco_status setup_ir(paco_handle* h) {
         CU(cudaStreamSynchronize(h->st));  // before J goes out of scope
     }
     if (h->mode != PACO_MODE_CLASSIC) {
-        CU(dalloc(&h->tl_city, (size_t)n * 2 * m));
+        CU(dalloc(&h->tl_city, (size_t)n * (2 * m + 1)));
         CU(dalloc(&h->tl_tau, (size_t)n * 2 * m));
-        CU(dalloc(&h->tl_count, n));
     }
     if (n <= 5000) {  // the reference keeps eta^beta in an f32 table for these sizes
         CU(dalloc(&h->eta_tab, (size_t)n * n));
@@ -769,7 +767,7 @@ static paco_status launch_ratios(paco_handle* h) {
         CU(cudaFuncSetAttribute(k_ir_touched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint32_t grid = std::min<uint32_t>(h->n, 8 * (uint32_t)h->num_sms);
     k_ir_touched<<<grid, 32, smem, h->st>>>(h->nbr, h->ratio, h->n, h->m, h->cfg.alpha, h->cfg.tau0, h->tl_city,
-                                            h->tl_tau, h->tl_count);
+                                            h->tl_tau);
     CU(cudaGetLastError());
     return PACO_OK;
 }
@@ -777,7 +775,7 @@ static paco_status launch_ratios(paco_handle* h) {
 static paco_status launch_construct_ir(paco_handle* h, bool seeding) {
     IrArgs a{};
     a.xy = h->xy; a.nbr = h->nbr; a.ratio = h->ratio;
-    a.tl_city = h->tl_city; a.tl_tau = h->tl_tau; a.tl_count = h->tl_count;
+    a.tl_city = h->tl_city; a.tl_tau = h->tl_tau;
     a.jump = h->ir_jump;
     a.T = h->mode == PACO_MODE_CLASSIC ? h->Tfull : nullptr;
     a.rng = h->rng; a.tours = h->tours; a.lb_sel = h->lb_sel; a.new_len = h->new_len;
