@@ -376,6 +376,7 @@ struct ConstructArgs {
     uint64_t stride;
     uint64_t seed, iter;
     uint32_t n, m, k, kp, nwords;  // kp = row stride of cand (k rounded up to even)
+    uint32_t sbe_words;            // words of the per-ant "superblock known empty" bitmap (0 = none)
     double eff_pp, mmf;
     int seeding;
     int validate;
@@ -535,7 +536,8 @@ __device__ __forceinline__ uint32_t free_bits_s(uint32_t vis_s, uint32_t w, uint
 }
 
 __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_t vis_s, uint32_t cur,
-                                                   uint32_t lane, uint32_t list_s, FbStats& fs) {
+                                                   uint32_t lane, uint32_t list_s, uint32_t sbe_s, bool sbe,
+                                                   FbStats& fs) {
     const double2 q = ldg_d2(a.xy + cur);  // issued with the F0 row: F1 needs it first
     {
         // lane l holds entries [E*l, E*l + E) of the sorted near list; the first unvisited
@@ -637,9 +639,15 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_
                 if (x >= 0 && y >= 0 && x < g.gws && y < g.ghs &&
                     (rho == 0 || !(rect_lb2(q, g.x0 + x * span, g.y0 + y * span, span, slack) > bound))) {
                     const uint32_t sbm = morton((uint32_t)x, (uint32_t)y);
-                    rs = ldg_u32(sb_start + sbm);
-                    re = ldg_u32(sb_start + sbm + 1);
-                    cand = range_has_unvisited_s(vis_s, rs, re);
+                    // a superblock found empty earlier in this construction stays empty (the
+                    // visited set only grows): its id range and bitmap words are not read again
+                    const bool known_empty = sbe && ((lds_u32(sbe_s + 4 * (sbm >> 5)) >> (sbm & 31)) & 1u);
+                    if (!known_empty) {
+                        rs = ldg_u32(sb_start + sbm);
+                        re = ldg_u32(sb_start + sbm + 1);
+                        cand = range_has_unvisited_s(vis_s, rs, re);
+                        red_or_shared_if(sbe_s + 4 * (sbm >> 5), 1u << (sbm & 31), sbe && !cand);
+                    }
                 }
             }
             unsigned ball = __ballot_sync(kFull, cand);
@@ -799,6 +807,11 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
     asm volatile("mov.b32 %0, %1;" : "=r"(vis_s) : "r"((uint32_t)__cvta_generic_to_shared(vis)));
     asm volatile("mov.b32 %0, %1;" : "=r"(fb_s) : "r"((uint32_t)__cvta_generic_to_shared(fb_list)));
     asm volatile("mov.b32 %0, %1;" : "=r"(warm_s) : "r"(((vis_s + nw * 4 + 15) & ~15u) + lane * 16));  // L1-warming scratch
+    // superblocks known to be empty (F1), after the warming scratch; cleared per construction
+    uint32_t sbe_s;
+    asm volatile("mov.b32 %0, %1;" : "=r"(sbe_s) : "r"(((vis_s + nw * 4 + 15) & ~15u) + 512));
+    for (uint32_t w = lane; w < a.sbe_words; w += 32) sts_u32_if(sbe_s + 4 * w, 0u, true);
+    __syncwarp();
     // lanes >= k never load: they hold (cur, 0.0f), and cur is always marked visited
     const bool lane_in = lane < k;
     const uint2* __restrict__ row_base = a.cand + lane;
@@ -938,7 +951,7 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
 #ifdef PACO_TIMING
                 const long long c0 = clock64();
 #endif
-                next = nearest_unvisited(fctx, vis_s, cur, lane, fb_s, fs);
+                next = nearest_unvisited(fctx, vis_s, cur, lane, fb_s, sbe_s, a.sbe_words != 0, fs);
                 tie_tol = -1.0f;
                 if (lane == 0) vis[next >> 5] |= 1u << (next & 31);
                 // fallbacks come in runs: pull the new city's near row from HBM into L2 now,

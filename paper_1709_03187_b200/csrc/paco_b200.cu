@@ -234,7 +234,12 @@ static size_t static_smem(const void* kern) {
     cudaFuncAttributes fa{};
     return cudaFuncGetAttributes(&fa, kern) == cudaSuccess ? fa.sharedSizeBytes : 0;
 }
-static size_t construct_dyn_smem(uint32_t nwords) { return kFbList * 4 + (size_t)nwords * 4 + 512 + 16; }
+// fallback list | visited bitmap | warming scratch | superblocks known to be empty (F1): the
+// grid has at most 16 n + 4096 cells (setup_grid), so at most n / 4 + 64 superblocks
+static uint32_t sbe_words_bound(uint32_t n) { return (n / 4 + 64 + 31) / 32; }
+static size_t construct_dyn_smem(uint32_t nwords, uint32_t sbe_words) {
+    return kFbList * 4 + (size_t)nwords * 4 + 512 + 16 + (size_t)sbe_words * 4;
+}
 static size_t construct_smem_need(uint32_t kp, uint32_t nwords, bool async_mode) {
     const void* kerns[4];
     int nk = 0;
@@ -250,7 +255,7 @@ static size_t construct_smem_need(uint32_t kp, uint32_t nwords, bool async_mode)
     }
     size_t st = 0;
     for (int q = 0; q < nk; ++q) st = std::max(st, static_smem(kerns[q]));
-    return construct_dyn_smem(nwords) + st;
+    return construct_dyn_smem(nwords, sbe_words_bound(nwords * 32)) + st;
 }
 // k_weights: ratios (8 B per ant) plus, on the hashed path, per thread 2^B slots and km sums
 static int weights_block(int km, bool hash) { return hash && km > 16 ? 128 : 256; }
@@ -805,6 +810,10 @@ static ConstructArgs construct_args(paco_handle* h, bool seeding) {
     a.words = h->cfg.draws == PACO_DRAWS_BUFFER ? h->words : nullptr;
     a.stride = h->words_stride; a.seed = h->cfg.seed; a.iter = h->iter;
     a.n = h->n; a.m = h->m; a.k = h->k; a.kp = h->kp; a.nwords = h->nwords;
+#ifndef PACO_NO_SB_EMPTY
+    a.sbe_words = ((h->g.ncells >> 6) + 31) / 32;
+    if (a.sbe_words > sbe_words_bound(h->n)) a.sbe_words = 0;
+#endif
     a.eff_pp = h->mode == PACO_MODE_PARTIAL ? h->cfg.partial_prob : 0.0;  // engine.hpp:164-165
     a.mmf = h->cfg.max_mod_frac;
     a.seeding = seeding ? 1 : 0;
@@ -817,7 +826,7 @@ static ConstructArgs construct_args(paco_handle* h, bool seeding) {
 
 static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint32_t blocks) {
     // shared memory: double-buffered stage of k candidate rows + the n-bit visited bitmap
-    const size_t smem = kFbList * 4 + (size_t)h->nwords * 4 + 512 + 16;  // fallback list + visited bitmap + scratch
+    const size_t smem = construct_dyn_smem(h->nwords, a.sbe_words);
     const bool buf = a.words != nullptr;
     // Shared-memory carveout: just enough for the CTAs one SM must host to run every ant at
     // once (ceil(m / #SMs) warps), so the rest of the unified L1 caches candidate rows.
@@ -838,7 +847,7 @@ static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint
 }
 
 static paco_status launch_construct_async(paco_handle* h, const ConstructArgs& a, uint32_t count) {
-    const size_t smem = kFbList * 4 + (size_t)h->nwords * 4 + 512 + 16;
+    const size_t smem = construct_dyn_smem(h->nwords, a.sbe_words);
     const int per_sm = (int)((h->m + h->num_sms - 1) / h->num_sms);
     const int carve = (int)std::min<size_t>(100, (size_t)per_sm * (smem + 1024) * 100 / (228 * 1024) + 1);
     const AsyncState st{h->nbr, h->lb_len, h->has_lb, h->lb_sel, h->gkey, h->improved};
