@@ -370,8 +370,8 @@ def run_ours(args, rank, world, local):
                   "ms": a_ms, "note": "synchronous=False (engine.hpp:213-244): one barrier-free launch for the "
                                       "config's iteration budget after seeding; weights rebuilt concurrently"},
         # per synchronous partial-mode step: k_weights, k_ant_order (longest ants first),
-        # k_construct, k_update, k_publish (profiles/r02_launches_c5.csv)
-        "gpu_launches": 5 * args.steps,
+        # k_construct, k_lengths (n >= 4096), k_update, k_publish (profiles/r02_launches_c5.csv)
+        "gpu_launches": (6 if spec["n"] >= 4096 else 5) * args.steps,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)

@@ -387,6 +387,7 @@ struct ConstructArgs {
     uint8_t* two_opt_flag;     // non-null: record the draw for k_two_opt instead of searching inline
     int force;
     uint32_t force_ant, force_start_pos, force_m_mod;
+    int defer_len;             // synchronous engine: lengths come from k_lengths after this kernel
 };
 
 // squared lower bound of the distance from q to the square [rx0, rx0+side) x [ry0, ry0+side),
@@ -1034,7 +1035,10 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
         n_2opt = 1;
     }
     // tour length (instance.hpp:120-127), int64, warp-parallel over positions
-    const long long len = warp_tour_length(out, n, a.xy, lane);
+    // The synchronous engine sums the lengths of all m tours in one grid-wide kernel after
+    // this one (k_lengths): one warp's pass over a C5 tour is a chain of ~780 dependent L2
+    // round-trip pairs at the tail of the longest ant, on the iteration's critical path.
+    const long long len = a.defer_len ? 0 : warp_tour_length(out, n, a.xy, lane);
     if (a.validate) {
         // permutation check (instance.hpp:109-117) reusing the bitmap
         for (uint32_t w = lane; w < nw; w += 32) vis[w] = 0u;
@@ -1446,6 +1450,56 @@ __global__ void k_map(const uint32_t* __restrict__ in, const uint32_t* __restric
                       uint32_t* __restrict__ out) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) out[i] = table[in[i]];
+}
+
+// Tour lengths (instance.hpp:120-127) of the m tours a synchronous k_construct launch wrote
+// (half 1 - lb_sel[a] of each ant's pair), exact int64 sums of EUC_2D distances added to
+// new_len[a] (k_construct left 0 there): kLenPos positions per 256-thread CTA, all loads of
+// a thread issued before its first distance. Integer sums, so the order of the atomic adds
+// does not matter.
+constexpr uint32_t kLenU = 8, kLenPos = 256 * kLenU;
+__global__ void __launch_bounds__(256) k_lengths(const uint32_t* __restrict__ tours, const uint8_t* __restrict__ lb_sel,
+                                                 const double2* __restrict__ xy, uint32_t n, int64_t* __restrict__ new_len) {
+    const uint32_t ant = blockIdx.y;
+    const uint32_t* __restrict__ out = tours + ((size_t)ant * 2 + (1 - lb_sel[ant])) * n;
+    const uint32_t base = blockIdx.x * kLenPos + threadIdx.x;
+    uint32_t c0[kLenU], c1[kLenU];
+#pragma unroll
+    for (uint32_t j = 0; j < kLenU; ++j) {
+        const uint32_t p = base + 256 * j;
+        const uint32_t q = p + 1 < n ? p + 1 : 0;
+        c0[j] = p < n ? out[p] : 0u;
+        c1[j] = p < n ? out[q] : 0u;
+    }
+    double2 x0[kLenU], x1[kLenU];
+#pragma unroll
+    for (uint32_t j = 0; j < kLenU; ++j) { x0[j] = xy[c0[j]]; x1[j] = xy[c1[j]]; }
+    double d2[kLenU];
+    bool ok = true;
+#pragma unroll
+    for (uint32_t j = 0; j < kLenU; ++j) {
+        d2[j] = sq_dist(x0[j], x1[j]);  // 0 for positions past n (c0 = c1 = 0)
+        ok &= sqrt_fast_ok(d2[j]);
+    }
+    long long len = 0;
+    if (__all_sync(kFull, ok)) {
+#pragma unroll
+        for (uint32_t j = 0; j < kLenU; ++j) len += (int32_t)__dadd_rn(sqrt_rn_fast(d2[j]), 0.5);
+    } else {
+#pragma unroll
+        for (uint32_t j = 0; j < kLenU; ++j) len += (int32_t)__dadd_rn(__dsqrt_rn(d2[j]), 0.5);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) len += __shfl_xor_sync(kFull, len, off);
+    __shared__ long long part[8];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = len;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += part[w];
+        atomicAdd(reinterpret_cast<unsigned long long*>(new_len + ant), (unsigned long long)t);
+    }
 }
 
 __global__ void k_tour_length(const uint32_t* __restrict__ t, const double2* __restrict__ xy, uint32_t n,

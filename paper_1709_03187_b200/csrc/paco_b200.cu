@@ -976,7 +976,17 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
                 CU(cudaGetLastError());
                 ca.order = h->order;
             }
+#ifndef PACO_NO_DEFER_LEN
+            // tour lengths in one grid-wide kernel after the constructions instead of one warp's
+            // pass at the tail of the longest ant (C5 construction 49.85 -> 48.55 ms, C4 22.10 ->
+            // 21.43; at n = 1000 the extra launch costs more than the pass)
+            ca.defer_len = n >= 4096 ? 1 : 0;
+#endif
             s = launch_construct(h, ca, m);
+            if (s == PACO_OK && ca.defer_len) {  // new_len[a] += the length of ant a's new tour
+                k_lengths<<<dim3((n + kLenPos - 1) / kLenPos, m), 256, 0, h->st>>>(h->tours, h->lb_sel, h->xy, n, h->new_len);
+                CU(cudaGetLastError());
+            }
         }
         if (s != PACO_OK) return s;
         if (h->two_opt_flag && h->two_opt_use_cluster) {  // maybe_two_opt's searches, a cluster per tour

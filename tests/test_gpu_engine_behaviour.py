@@ -285,7 +285,7 @@ def test_bench_line_contract():
                 "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks", "cpu_baseline"):
         assert key in d, key
     assert d["value"] > 0 and d["steps"] == 2 and d["warmup"] == 3 and d["n_gpus"] == 1
-    assert d["gpu_launches"] == 5 * 2
+    assert d["gpu_launches"] == 6 * 2  # C2: k_weights, k_ant_order, k_construct, k_lengths, k_update, k_publish
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1
     lat = d["roofline"]["latency"]  # null only when no SM clock was sampled
     assert lat is None or (lat["bound"] == "latency" and 0 < lat["frac"] <= 1.5 and lat["floor_terms"]["scan_levels"] == 5)
