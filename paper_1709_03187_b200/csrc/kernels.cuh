@@ -388,6 +388,7 @@ struct ConstructArgs {
     int force;
     uint32_t force_ant, force_start_pos, force_m_mod;
     int defer_len;             // synchronous engine: lengths come from k_lengths after this kernel
+    unsigned int* qhead;       // non-null: CTAs keep taking the next position of `order` (starts at gridDim.x)
 };
 
 // squared lower bound of the distance from q to the square [rx0, rx0+side) x [ry0, ry0+side),
@@ -1082,32 +1083,45 @@ __global__ void __launch_bounds__(32, 1) k_construct(ConstructArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];  // fallback list | visited bitmap | warm scratch
     __shared__ FallbackCtx fctx;
     init_fallback_ctx(a, fctx);
-    const uint32_t ant = a.force ? a.force_ant : (a.order ? a.order[blockIdx.x] : blockIdx.x);
-    bool partial;
-    uint32_t cnt[5];
+    uint32_t slot = blockIdx.x;
+    // one ant per CTA, or (qhead) the next position of the launch order until none is left
+    for (;;) {
+        const uint32_t ant = a.force ? a.force_ant : (a.order ? a.order[slot] : slot);
+        bool partial;
+        uint32_t cnt[5];
 #ifdef PACO_ANTPROF
-    const unsigned long long pt0 = gtimer();
+        const unsigned long long pt0 = gtimer();
 #endif
-    const long long len = build_one<KP, STEPS, BUF>(a, ant, a.iter, a.seeding != 0, smem_raw, fctx, partial, cnt);
+        const long long len = build_one<KP, STEPS, BUF>(a, ant, a.iter, a.seeding != 0, smem_raw, fctx, partial, cnt);
 #ifdef PACO_ANTPROF
-    if (threadIdx.x == 0 && ant < 4096) {
-        uint32_t smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        unsigned long long* g = g_ant + 6 * ant;
-        g[0] = pt0; g[1] = gtimer(); g[2] = smid; g[3] = cnt[0]; g[4] = cnt[1]; g[5] = partial;
-    }
-#endif
-    if (threadIdx.x == 0) {
-        a.new_len[ant] = len;
-        if (!a.force) {
-            a.partial_flag[ant] = partial ? 1 : 0;
-            atomicAdd(&a.counters[0], (unsigned long long)cnt[0]);
-            atomicAdd(&a.counters[1], (unsigned long long)cnt[1]);
-            atomicAdd(&a.counters[2], (unsigned long long)cnt[2]);
-            atomicAdd(&a.counters[3], (unsigned long long)cnt[3]);
-            atomicAdd(&a.counters[partial ? 5 : 4], 1ull);
-            if (cnt[4]) atomicAdd(&a.counters[9], 1ull);
+        if (threadIdx.x == 0 && ant < 4096) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            unsigned long long* g = g_ant + 6 * ant;
+            uint32_t wid;
+            asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+            g[0] = pt0; g[1] = gtimer(); g[2] = smid | (wid << 16); g[3] = cnt[0]; g[4] = cnt[1]; g[5] = partial;
         }
+#endif
+        if (threadIdx.x == 0) {
+            a.new_len[ant] = len;
+            if (!a.force) {
+                a.partial_flag[ant] = partial ? 1 : 0;
+                atomicAdd(&a.counters[0], (unsigned long long)cnt[0]);
+                atomicAdd(&a.counters[1], (unsigned long long)cnt[1]);
+                atomicAdd(&a.counters[2], (unsigned long long)cnt[2]);
+                atomicAdd(&a.counters[3], (unsigned long long)cnt[3]);
+                atomicAdd(&a.counters[partial ? 5 : 4], 1ull);
+                if (cnt[4]) atomicAdd(&a.counters[9], 1ull);
+            }
+        }
+        if (!a.qhead) break;
+        uint32_t nxt = 0;
+        if (threadIdx.x == 0) nxt = atomicAdd(a.qhead, 1u);
+        nxt = __shfl_sync(kFull, nxt, 0);
+        if (nxt >= a.m) break;
+        slot = nxt;
+        __syncwarp();
     }
 }
 
@@ -1404,8 +1418,10 @@ __global__ void __launch_bounds__(512, 1) k_two_opt_cluster(uint32_t* __restrict
 // keys over the next power of two >= m (m <= 4096; larger colonies keep the identity).
 __global__ void __launch_bounds__(1024) k_ant_order(const uint32_t* __restrict__ words, uint64_t stride,
                                                     uint64_t seed, uint64_t iter, uint32_t n, uint32_t m,
-                                                    double eff_pp, double mmf, int seeding, uint32_t* __restrict__ order) {
+                                                    double eff_pp, double mmf, int seeding, uint32_t* __restrict__ order,
+                                                    unsigned int* qhead, unsigned int qstart) {
     __shared__ unsigned long long key[4096];
+    if (qhead && threadIdx.x == 0) *qhead = qstart;
     uint32_t P = 1;
     while (P < m) P <<= 1;
     const uint2 k2 = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));

@@ -118,6 +118,7 @@ struct paco_handle {
     float* eta = nullptr;
     uint2* cand = nullptr;
     uint32_t* order = nullptr;  // CTA -> ant launch order of K2 (k_ant_order), m <= 4096
+    unsigned int* qhead = nullptr;  // next position of `order` to hand out (persistent K2 CTAs)
     uint32_t* tours = nullptr;
     uint8_t *lb_sel = nullptr, *has_lb = nullptr, *improved = nullptr, *partial = nullptr;
     int64_t *new_len = nullptr, *lb_len = nullptr, *g_len = nullptr;
@@ -154,7 +155,7 @@ struct paco_handle {
         if (st) cudaStreamSynchronize(st);  // nothing may still use the buffers returned below
         if (st2) cudaStreamSynchronize(st2);
         void* ptrs[] = {xy, orig_of, int_of, cell_start, sb_start, knn, eta, cand, tours, lb_sel, has_lb, improved,
-                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words, order, two_opt_flag, two_opt_edges, two_opt_txy,
+                        partial, new_len, lb_len, g_len, nbr, cur_nbr, T, gb, gkey, counters, err, words, order, qhead, two_opt_flag, two_opt_edges, two_opt_txy,
                         scratch_u32, scratch_u64, rng, ratio, tl_city, tl_tau, ir_jump, Tfull, eta_tab, cand_mult};
         for (void* p : ptrs) dfree(p);
         for (auto e : evpool) cudaEventDestroy(e);
@@ -374,7 +375,7 @@ static paco_status alloc_colony(paco_handle* h) {
     CU(cudaMemsetAsync(h->err, 0, sizeof(int), st));
     if (h->mode == PACO_MODE_CLASSIC) CU(dalloc(&h->cur_nbr, (size_t)m * n));
 #ifndef PACO_NO_ORDER
-    if (!h->ir && !h->async_mode && m <= 4096) CU(dalloc(&h->order, m));
+    if (!h->ir && !h->async_mode && m <= 4096) { CU(dalloc(&h->order, m)); CU(dalloc(&h->qhead, 1)); }
 #endif
     if (!h->ir && !h->async_mode && h->cfg.two_opt_prob > 0.0) {
         h->two_opt_ctas = std::min<uint32_t>(m, 64);
@@ -831,7 +832,10 @@ static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint
     // Shared-memory carveout: just enough for the CTAs one SM must host to run every ant at
     // once (ceil(m / #SMs) warps), so the rest of the unified L1 caches candidate rows.
     const int per_sm = (int)((blocks + h->num_sms - 1) / h->num_sms);
-    const int carve = (int)std::min<size_t>(100, (size_t)per_sm * (smem + 1024) * 100 / (228 * 1024) + 1);
+    int carve = (int)std::min<size_t>(100, (size_t)per_sm * (smem + 1024) * 100 / (228 * 1024) + 1);
+#ifdef PACO_CARVE_ENV
+    if (const char* e = getenv("PACO_CARVE")) carve = atoi(e);
+#endif
     auto launch = [&](auto kern) -> paco_status {
         if (smem > 48 * 1024)
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -970,11 +974,27 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
             s = launch_construct_ir(h, seeding);
         } else {
             ConstructArgs ca = construct_args(h, seeding);
+            uint32_t blocks = m;
             if (h->order && !seeding && h->mode == PACO_MODE_PARTIAL) {  // longest ants first (k_ant_order)
+                // Persistent CTAs: with more than kQueueSlots ants per SM, only kQueueSlots CTAs per
+                // SM are launched and each takes the next-longest ant when its own is done. The
+                // chain of a decision slows by ~4 ns per co-resident warp and by ~13 ns when two
+                // warps share a scheduler (profiles/README.md); five resident warps instead of
+                // seven-decaying-to-one measured best (C5 47.42 -> 46.86 ms; 4: 47.2 and uneven,
+                // 6: 47.09, 3: 60.6).
+                constexpr uint32_t kQueueSlots = 5;
+                uint32_t qstart = m >= (kQueueSlots + 1) * (uint32_t)h->num_sms ? kQueueSlots * (uint32_t)h->num_sms : 0;
+#ifdef PACO_NO_QUEUE
+                qstart = 0;
+#endif
+#ifdef PACO_QUEUE_ENV
+                if (const char* e = getenv("PACO_SLOTS")) qstart = std::min<uint32_t>(m, (uint32_t)atoi(e) * (uint32_t)h->num_sms);
+#endif
                 k_ant_order<<<1, 1024, 0, h->st>>>(ca.words, ca.stride, h->cfg.seed, h->iter, n, m, ca.eff_pp, ca.mmf,
-                                                   0, h->order);
+                                                   0, h->order, qstart ? h->qhead : nullptr, qstart);
                 CU(cudaGetLastError());
                 ca.order = h->order;
+                if (qstart) { ca.qhead = h->qhead; blocks = qstart; }
             }
 #ifndef PACO_NO_DEFER_LEN
             // tour lengths in one grid-wide kernel after the constructions instead of one warp's
@@ -982,7 +1002,7 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
             // 21.43; at n = 1000 the extra launch costs more than the pass)
             ca.defer_len = n >= 4096 ? 1 : 0;
 #endif
-            s = launch_construct(h, ca, m);
+            s = launch_construct(h, ca, blocks);
             if (s == PACO_OK && ca.defer_len) {  // new_len[a] += the length of ant a's new tour
                 k_lengths<<<dim3((n + kLenPos - 1) / kLenPos, m), 256, 0, h->st>>>(h->tours, h->lb_sel, h->xy, n, h->new_len);
                 CU(cudaGetLastError());
