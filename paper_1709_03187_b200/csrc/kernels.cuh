@@ -1478,23 +1478,29 @@ __global__ void __launch_bounds__(256) k_lengths(const uint32_t* __restrict__ to
                                                  const double2* __restrict__ xy, uint32_t n, int64_t* __restrict__ new_len) {
     const uint32_t ant = blockIdx.y;
     const uint32_t* __restrict__ out = tours + ((size_t)ant * 2 + (1 - lb_sel[ant])) * n;
-    const uint32_t base = blockIdx.x * kLenPos + threadIdx.x;
-    uint32_t c0[kLenU], c1[kLenU];
+    // kLenU consecutive positions per thread: position p's second city is position p + 1's
+    // first, so a thread gathers kLenU + 1 coordinates for kLenU distances
+    const uint32_t p0 = (blockIdx.x * 256 + threadIdx.x) * kLenU;
+    uint32_t c[kLenU + 1];
+    if ((n & 3u) == 0 && p0 + kLenU <= n) {  // 16-byte aligned rows: two vector loads
+        const uint4 v0 = *reinterpret_cast<const uint4*>(out + p0), v1 = *reinterpret_cast<const uint4*>(out + p0 + 4);
+        c[0] = v0.x; c[1] = v0.y; c[2] = v0.z; c[3] = v0.w; c[4] = v1.x; c[5] = v1.y; c[6] = v1.z; c[7] = v1.w;
+        c[kLenU] = out[p0 + kLenU < n ? p0 + kLenU : 0];
+    } else {
 #pragma unroll
-    for (uint32_t j = 0; j < kLenU; ++j) {
-        const uint32_t p = base + 256 * j;
-        const uint32_t q = p + 1 < n ? p + 1 : 0;
-        c0[j] = p < n ? out[p] : 0u;
-        c1[j] = p < n ? out[q] : 0u;
+        for (uint32_t j = 0; j <= kLenU; ++j) {
+            const uint32_t p = p0 + j;
+            c[j] = p < n ? out[p] : (p == n ? out[0] : 0u);
+        }
     }
-    double2 x0[kLenU], x1[kLenU];
+    double2 x[kLenU + 1];
 #pragma unroll
-    for (uint32_t j = 0; j < kLenU; ++j) { x0[j] = xy[c0[j]]; x1[j] = xy[c1[j]]; }
+    for (uint32_t j = 0; j <= kLenU; ++j) x[j] = xy[c[j]];
     double d2[kLenU];
     bool ok = true;
 #pragma unroll
     for (uint32_t j = 0; j < kLenU; ++j) {
-        d2[j] = sq_dist(x0[j], x1[j]);  // 0 for positions past n (c0 = c1 = 0)
+        d2[j] = p0 + j < n ? sq_dist(x[j], x[j + 1]) : 0.0;
         ok &= sqrt_fast_ok(d2[j]);
     }
     long long len = 0;

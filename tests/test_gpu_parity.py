@@ -201,6 +201,16 @@ def test_candidate_counts(n, k):
     lockstep(inst, 5, ants=8, candidates=k, seed=k + 1)
 
 
+@pytest.mark.parametrize("n", [4096, 4099, 6150, 8193])
+def test_deferred_length_kernel_edges(n):
+    """From n = 4096 the synchronous engine sums tour lengths in k_lengths after the
+    constructions (instance.hpp:120-127): rows that are and are not 16-byte aligned (n mod 4),
+    a last CTA that is full, nearly empty or one position long; lengths, l_best and g_best in
+    lockstep with O2."""
+    inst = make_config_instance("C1", n=n)
+    lockstep(inst, 4, ants=12, candidates=16, seed=n)
+
+
 def test_duplicates_and_collinear():
     xs = np.array([5.0] * 40 + list(range(60)), dtype=float)
     ys = np.array([5.0] * 40 + [0.0] * 60, dtype=float)
