@@ -168,6 +168,22 @@ def test_validation_buffer_draws():
     lockstep(inst, 6, ants=16, candidates=12, words_fn=words)
 
 
+@pytest.mark.parametrize("draws,n,p2", [("philox", 500, 0.0), ("buffer", 300, 0.0), ("philox", 4100, 0.05)])
+def test_persistent_queue_colonies(draws, n, p2):
+    """Colonies above five ants per SM (900 ants on a 148-SM B200) run K2 as persistent CTAs
+    that take the ants longest first from the k_ant_order queue: Philox and validation-buffer
+    draws, the in-kernel and the deferred (n >= 4096) length paths, 2-opt flags, in lockstep
+    with O2 (construction.hpp:283-365 for every ant, whatever CTA builds it)."""
+    rng = np.random.default_rng(9)
+
+    def words(it, m, stride):
+        return rng.integers(0, 2**32, size=(m, stride), dtype=np.uint64).astype(np.uint32)
+
+    inst = make_config_instance("C1", n=n)
+    lockstep(inst, 4, ants=900, candidates=16, seed=3, words_fn=words if draws == "buffer" else None,
+             two_opt_prob=p2, two_opt_window=10)
+
+
 def test_alpha_beta_integer_powers():
     inst = make_config_instance("C1", n=400)
     lockstep(inst, 8, ants=8, candidates=10, alpha=5.0, beta=5.0, seed=11)
