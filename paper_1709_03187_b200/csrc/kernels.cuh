@@ -402,6 +402,7 @@ __device__ __forceinline__ double rect_lb2(double2 q, double rx0, double ry0, do
 struct FbStats {
 #ifdef PACO_TIMING
     long long searches = 0, rings = 0, sbs = 0, cities = 0, t_test = 0, t_scan = 0, t_argmin = 0, t_pre = 0;
+    long long f0_n = 0, f0_row = 0, f0_probe = 0, f0_redux = 0;  // F0 anatomy: near row, bitmap probes, reduction
 #endif
 };
 
@@ -546,6 +547,9 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_
         // entry overall is one integer min-reduction over (entry index, city) keys
         constexpr uint32_t E = kNearRow / 32;
         uint32_t c[E];
+#ifdef PACO_TIMING
+        const long long f0a = clock64();
+#endif
         const uint32_t* row = a.knn32 + (size_t)cur * kNearRow + E * lane;
         if constexpr (E == 1) {
             c[0] = ldg_u32(row);
@@ -561,6 +565,9 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_
             c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
             c[4] = w.x; c[5] = w.y; c[6] = w.z; c[7] = w.w;
         }
+#ifdef PACO_TIMING
+        long long f0b; asm volatile("mov.u64 %0, %%clock64;" : "=l"(f0b) : "r"(c[0] ^ c[E - 1]));
+#endif
         uint32_t key = kNone;
 #pragma unroll
         for (int s = E - 1; s >= 0; --s) {
@@ -568,7 +575,14 @@ __device__ PACO_FB_ATTR uint32_t nearest_unvisited(const FallbackCtx& a, uint32_
             const uint32_t vw = lds_u32_if(vis_s + ((c[s] >> 5) << 2), ok, ~0u);
             if (ok && !((vw >> (c[s] & 31)) & 1u)) key = ((E * lane + s) << 21) | c[s];
         }
+#ifdef PACO_TIMING
+        long long f0c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(f0c) : "r"(key));
+#endif
         const uint32_t km = __reduce_min_sync(kFull, key);
+#ifdef PACO_TIMING
+        long long f0d; asm volatile("mov.u64 %0, %%clock64;" : "=l"(f0d) : "r"(km));
+        ++fs.f0_n; fs.f0_row += f0b - f0a; fs.f0_probe += f0c - f0b; fs.f0_redux += f0d - f0c;
+#endif
         if (km != kNone) return km & 0x1fffffu;
     }
 #ifdef PACO_TIMING
@@ -1006,6 +1020,8 @@ __device__ __forceinline__ long long build_one(const ConstructArgs& a, uint32_t 
 #ifdef PACO_TIMING
     if (lane == 0) {
         atomicAdd(&g_timing[0], (unsigned long long)(clock64() - loop0));
+        atomicAdd(&g_timing[4], (unsigned long long)fs.f0_n); atomicAdd(&g_timing[5], (unsigned long long)fs.f0_row);
+        atomicAdd(&g_timing[6], (unsigned long long)fs.f0_probe); atomicAdd(&g_timing[7], (unsigned long long)fs.f0_redux);
         atomicAdd(&g_timing[1], (unsigned long long)fbc);
         atomicAdd(&g_timing[2], (unsigned long long)n_dec);
     }

@@ -32,6 +32,8 @@ for it in range(3):
            "loop_cycles": int(t[0]), "fallback_cycles": int(t[1]), "decisions": int(t[2]),
            "f1_searches": int(t[9]), "f1_rings": int(t[10]), "f1_sbs": int(t[11]), "f1_cities": int(t[12]),
            "f1_test": int(t[13]), "f1_scan": int(t[14]), "f1_argmin": int(t[15]), "f1_pre": int(t[3]),
+           "f0": {"n": int(t[4]), "row_cycles": round(t[5] / max(1, t[4]), 1), "probe_cycles": round(t[6] / max(1, t[4]), 1),
+                  "redux_cycles": round(t[7] / max(1, t[4]), 1), "fallback_cycles_each": round(t[1] / max(1, t[4]), 1)},
            "crit_total_mcycles": round(cyc.sum() / 1e6, 2), "crit_fallbacks": int(fb.sum()),
            "crit_f1": int(f1.sum()),
            "crit_buckets": [(round(c / 1e6, 2), int(f), int(s), int(r)) for c, f, s, r in zip(cyc, fb, f1, rings)]}
