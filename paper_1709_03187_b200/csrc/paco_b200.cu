@@ -827,7 +827,7 @@ static ConstructArgs construct_args(paco_handle* h, bool seeding) {
 
 static paco_status launch_construct(paco_handle* h, const ConstructArgs& a, uint32_t blocks) {
     // shared memory: double-buffered stage of k candidate rows + the n-bit visited bitmap
-    const size_t smem = construct_dyn_smem(h->nwords, a.sbe_words);
+    const size_t smem = construct_dyn_smem(h->nwords, a.sbe_words) + (size_t)a.sb_words * 4;
     const bool buf = a.words != nullptr;
     // Shared-memory carveout: just enough for the CTAs one SM must host to run every ant at
     // once (ceil(m / #SMs) warps), so the rest of the unified L1 caches candidate rows.
@@ -995,6 +995,12 @@ paco_status paco_iterate(paco_handle* h, uint64_t count) {
                 CU(cudaGetLastError());
                 ca.order = h->order;
                 if (qstart) { ca.qhead = h->qhead; blocks = qstart; }
+                // the superblock-start table rides in the shared memory five CTAs per SM leave free
+                if (qstart) {
+                    const size_t sbw = (size_t)(h->g.ncells >> 6) + 1;
+                    const size_t per_cta = construct_dyn_smem(h->nwords, ca.sbe_words) + sbw * 4 + 1024 + 256;
+                    if (sbw <= 3072 && per_cta * kQueueSlots <= 227 * 1024) ca.sb_words = (uint32_t)sbw;
+                }
             }
 #ifndef PACO_NO_DEFER_LEN
             // tour lengths in one grid-wide kernel after the constructions instead of one warp's
